@@ -1,0 +1,321 @@
+#!/usr/bin/env python3
+"""GPops/s of the tree-evaluation hot path on B200 (BASELINE.json metric).
+
+Workload (config.workload = "c3"): BASELINE.json configs[2] — the
+evaluation-only batch of 4000 seeded random prefix trees, node counts
+log-uniform in [10^4, 10^6] (~8.6e8 nodes, ~4.1e10 GPops), ops uniform over
+{+,-,*,/}, leaves 50% x / 50% constants in [-1,1], 48 Sextic fitness cases.
+It is the largest config that is a pure pass of the hot path over one batch;
+configs[1] (pop 4000 evolution) is a parity case whose per-generation work is
+microseconds.
+
+One step = evaluate_population over the whole batch (per-case outputs, MAE
+fitness, hits, size, depth of every tree). With --gpus N (torchrun, one
+process per GPU) the population is N config-3 batches, one per rank (rank r
+uses corpus seed SEED + r): weak scaling, fixed work per GPU. Every step ends
+with an NCCL all-gather of the 16-byte per-individual records, so every rank
+holds the whole population's fitness for tournament selection.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SEED = 1
+M_TREES = 4000
+LG_LO, LG_HI = 4.0, 6.0
+LANES = 48
+METRIC = "GPops/s (tree nodes x fitness cases evaluated per sec)"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 9:
+                for k, nm in enumerate(names):
+                    if r[5 + k].lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def oracle_sample(threads, seconds_target, first_trees=None):
+    """Time the oracle's multi-threaded evaluate_population (the reference's
+    CPU algorithm as restated in oracle/) on a prefix of the workload."""
+    import paper_1902_09215_b200 as ltgp
+    from tests._oracle import load_oracle
+
+    o = load_oracle()
+    suite = ltgp.make_suite(ltgp.suite_seed(SEED))
+    sizes = ltgp.corpus_sizes(SEED, M_TREES, LG_LO, LG_HI)
+    # calibrate on the first few trees
+    n_cal = 8
+    buf, offs, sz = ltgp.corpus(SEED, M_TREES, LG_LO, LG_HI, first=0, n=n_cal)
+    t0 = time.perf_counter()
+    o.evaluate_population(buf, offs, sz, suite, threads=threads)
+    rate = float(sz.sum()) / max(time.perf_counter() - t0, 1e-6)  # nodes/s
+    budget = rate * seconds_target
+    if first_trees is None:
+        csum = np.cumsum(sizes.astype(np.float64))
+        first_trees = int(min(M_TREES, max(n_cal, np.searchsorted(csum, budget) + 1)))
+    buf, offs, sz = ltgp.corpus(SEED, M_TREES, LG_LO, LG_HI, first=0, n=first_trees)
+    return o, suite, buf, offs, sz, first_trees
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    per_step = max(2.0, min(10.0, 150.0 / max(1, args.steps + args.warmup)))
+    o, suite, buf, offs, sz, ntrees = oracle_sample(threads, per_step)
+    nodes = int(sz.sum())
+    for _ in range(args.warmup):
+        o.evaluate_population(buf, offs, sz, suite, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        o.evaluate_population(buf, offs, sz, suite, threads=threads)
+    dt = time.perf_counter() - t0
+    value = nodes * LANES * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GPops/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded config-3 corpus)",
+        "config": {"workload": "c3", "trees": M_TREES, "lg_nodes": [LG_LO, LG_HI], "seed": SEED,
+                   "sample_trees": ntrees, "sample_nodes": nodes},
+        "cpu_baseline": {"value": value, "unit": "GPops/s", "cores": threads, "kind": "port",
+                         "sample": f"first {ntrees} of {M_TREES} config-3 trees ({nodes} nodes) per step; "
+                                   f"oracle eval_batch (48-lane AVX frames) on a {threads}-thread dynamic pool"},
+        "e2e": {"value": value, "unit": "GPops/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1902_09215_b200 as ltgp
+    from paper_1902_09215_b200.sharding import DeviceRecords
+
+    torch.cuda.set_device(local_rank)
+    pk, pk_kind = peaks()
+    # weak scaling: rank r owns population slots [r*M, (r+1)*M), a config-3
+    # batch generated from corpus seed SEED + r
+    ranges = [(r * M_TREES, M_TREES) for r in range(world)]
+    first, count = 0, M_TREES
+    nodes_job = sum(int(ltgp.corpus_sizes(SEED + r, M_TREES, LG_LO, LG_HI).sum()) for r in range(world))
+    bytes_job = sum(int(((ltgp.corpus_sizes(SEED + r, M_TREES, LG_LO, LG_HI) + 15) // 16 * 16).sum())
+                    for r in range(world))
+    pinned_keep = []
+
+    def pinned(nbytes):
+        t = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        pinned_keep.append(t)
+        return t.numpy()
+
+    buf, offs, sizes = ltgp.corpus(SEED + rank, M_TREES, LG_LO, LG_HI, pinned=pinned, first=first, n=count)
+    nodes_rank = int(sizes.sum())
+    suite = ltgp.make_suite(ltgp.suite_seed(SEED))
+    e = ltgp.Engine([local_rank], node_limit=15_000_000)
+    e.set_suite(*suite)
+    e.upload_packed(buf, offs, sizes)
+    rec = np.zeros(count, ltgp.RECORD_DTYPE)
+    dptr, _, _, sptr = e.shard_records(0)
+    estream = torch.cuda.ExternalStream(sptr)
+    cmax = max(c for _, c in ranges)
+    gather_out = torch.empty(world * cmax * 16, dtype=torch.uint8, device="cuda")
+    gather_in = torch.zeros(cmax * 16, dtype=torch.uint8, device="cuda")
+
+    def step(host_records=True):
+        e.evaluate_launch()
+        e.evaluate_collect(rec if host_records else None)
+        if world > 1:  # records of every shard to every rank (NCCL over NVLink)
+            dev_rec = torch.as_tensor(DeviceRecords(dptr, count), device="cuda")
+            gather_in[: count * 16].copy_(dev_rec)
+            dist.all_gather_into_tensor(gather_out, gather_in)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3) if args.warmup >= 0 else 3):
+        step()
+    # ---------------- device-resident throughput (value) ----------------
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(estream)
+    kern = []
+    comb = []
+    launches = 0
+    for _ in range(args.steps):
+        step()
+        st = e.stats()
+        kern.append(st["eval_kernel_seconds"])
+        comb.append(st["combine_seconds"])
+        launches += st["kernel_launches"]
+    ev1.record(torch.cuda.current_stream())
+    barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    t_max = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms = float(t_max.item())
+    value = nodes_job * LANES * args.steps / (ms * 1e-3)
+    kern_s = float(np.mean(kern))
+    # ---------------- end to end through the C ABI (e2e) ----------------
+    barrier()
+    ev2 = torch.cuda.Event(enable_timing=True)
+    ev3 = torch.cuda.Event(enable_timing=True)
+    ev2.record(estream)
+    for _ in range(args.steps):
+        e.upload_packed(buf, offs, sizes)       # H2D of the step's trees from pinned memory
+        step(host_records=True)                 # evaluate + D2H of the records
+    ev3.record(torch.cuda.current_stream())
+    barrier()
+    ms_e2e = ev2.elapsed_time(ev3)
+    t_e2e = torch.tensor([ms_e2e], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
+    ms_e2e = float(t_e2e.item())
+    e2e = nodes_job * LANES * args.steps / (ms_e2e * 1e-3)
+    # ---------------- roofline of the dominant kernel (k_eval) ----------------
+    sms = torch.cuda.get_device_properties(local_rank).multi_processor_count
+    peak_tops = sms * 128 * pk["sm_max_mhz"] * 1e6 / 1e12  # FP32 lanes/clk x clock, 1 GPop = 1 op
+    achieved = nodes_rank * LANES / kern_s / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_k_eval.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": "GPops/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded config-3 corpus, generated on the host)",
+        "config": {"workload": "c3", "trees_per_gpu": M_TREES, "lg_nodes": [LG_LO, LG_HI],
+                   "seeds": [SEED + r for r in range(world)],
+                   "nodes": nodes_job, "gpops_per_step": nodes_job * LANES,
+                   "parallelism": f"population shards x{world}" + (" + NCCL all-gather of records" if world > 1 else ""),
+                   "l2": "inputs larger than L2: %.0f MB of opcodes per GPU vs 126 MB L2" % (nodes_rank / 1e6)},
+        "e2e": {"value": e2e, "unit": "GPops/s", "h2d_bytes_per_step": bytes_job,
+                "d2h_bytes_per_step": M_TREES * 16 * world},
+        "gpu_launches": launches,
+        "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak_tops, "unit": "TFLOP/s",
+                     "frac": achieved / peak_tops, "traffic": traffic,
+                     "note": f"k_eval only: {nodes_rank} nodes x 48 ops / {kern_s * 1e3:.3f} ms avg launch; "
+                             f"peak = {sms} SMs x 128 FP32 lanes x {pk['sm_max_mhz']:.0f} MHz ({pk_kind} clock); "
+                             f"opcode stream {nodes_rank / kern_s / 1e9:.1f} GB/s of {pk['hbm_gbs']:.0f} GB/s HBM ({pk_kind})",
+                     "combine_ms": float(np.mean(comb)) * 1e3},
+        "clocks": clk,
+    }
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        o, s2, cb, co, cs, ntrees = oracle_sample(threads, args.cpu_seconds)
+        t0 = time.perf_counter()
+        o.evaluate_population(cb, co, cs, s2, threads=threads)
+        dt = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": float(cs.sum()) * LANES / dt, "unit": "GPops/s", "cores": threads,
+                                "kind": "port",
+                                "sample": f"first {ntrees} of {M_TREES} config-3 trees ({int(cs.sum())} nodes); "
+                                          f"oracle eval_batch on a {threads}-thread pool, {dt:.1f} s"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    e.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,139 @@
+/*
+ * ltgp_cuda.h — C ABI of the B200 fitness-evaluation engine (libltgp_cuda.so).
+ *
+ * This is the drop-in boundary for the reference's population API
+ * (/root/reference/proj/include/ltgp/evolve.hpp:95-117 and eval.hpp:65-87).
+ * Every entry point below names the reference declaration it replaces.
+ * Plain C types only: no exceptions, no C++ or torch types cross it.
+ *
+ * Conventions:
+ *  - every call returns int status: 0 = ok, < 0 = error (ltgp_last_error()
+ *    has the message). A crossover reaching the node limit is NOT an error:
+ *    it is reported through an out-flag, like CrossoverResult::size_limit_hit
+ *    (genome.hpp:71-74) and ExecOutcome::size_limit_hit (evolve.hpp:102-104).
+ *  - the caller owns host arrays; the engine owns device arenas and genomes
+ *    by population slot.
+ *  - one coordinator thread per engine handle (the reference's sequential
+ *    coordinator). Shards of the population may live on
+ *    several GPUs (devices[]); the engine uses one CUDA stream per shard.
+ */
+#ifndef LTGP_CUDA_H
+#define LTGP_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LTGP_LANES 48       /* kLaneWidth, common.hpp:10-11 */
+#define LTGP_CONSTANTS 250  /* kConstantCount, opcodes.hpp:18 */
+#define LTGP_MAX_SHARDS 16
+
+typedef struct ltgp_engine ltgp_engine;
+
+/* Per-individual record: Individual minus the genome (evolve.hpp:17-23). */
+typedef struct {
+    float fitness;  /* MAE, sequential lane order (eval.hpp:81-84); NaN possible */
+    int32_t hits;   /* lanes with |o-t| <= 0.01f (eval.hpp:86-87) */
+    uint32_t size;  /* nodes */
+    uint32_t depth; /* single node = 1 (genome.hpp:45-46) */
+} ltgp_record;
+
+/* CrossoverPlan (evolve.hpp:25-32). */
+typedef struct {
+    uint32_t mum_index, dad_index, mum_pt, dad_pt;
+} ltgp_plan;
+
+typedef struct {
+    int n_shards;                     /* 1..LTGP_MAX_SHARDS */
+    int devices[LTGP_MAX_SHARDS];     /* CUDA ordinal per shard (may repeat) */
+    uint64_t node_limit;              /* RunConfig::node_limit (evolve.hpp:40) */
+    uint64_t arena_bytes;             /* per shard and buffer; 0 = grow on demand */
+    uint32_t chunk_nodes;             /* intra-tree chunk length; 0 = default */
+    int use_nccl;                     /* 1: NCCL all-gather when devices are distinct */
+} ltgp_config;
+
+/* Counters (GpopsCounter, eval.hpp:14-25, plus device timings). */
+typedef struct {
+    uint64_t nodes_evaluated;   /* sum of sizes over all evaluations */
+    double eval_seconds;        /* device time of the last evaluation (CUDA events) */
+    double eval_kernel_seconds; /* of which the chunk/tree scan kernel (k_eval) */
+    double combine_seconds;     /* of which the spine combine kernel (k_combine) */
+    double splice_seconds;      /* device time of the last extent+splice */
+    double gather_seconds;      /* device time of the last record all-gather */
+    uint64_t arena_high_water;  /* bytes, max over shards */
+    uint64_t last_chunks;       /* chunk work items of the last evaluation */
+    uint64_t last_fallback_items; /* items re-run on the deep-stack path */
+    uint32_t kernel_launches;   /* engine kernels launched by the last call */
+} ltgp_stats;
+
+const char* ltgp_last_error(void);
+const char* ltgp_version(void);
+
+int ltgp_engine_create(const ltgp_config* cfg, ltgp_engine** out);
+int ltgp_engine_destroy(ltgp_engine* e);
+
+/* TestSuite (sextic.hpp:25-31): 48 inputs, 48 targets, 250 constants. */
+int ltgp_set_suite(ltgp_engine* e, const float* inputs48, const float* targets48,
+                   const float* consts250);
+
+/* Replace the current population by M host genomes (pointer per genome),
+   e.g. the ramped_half_and_half output (genome.hpp:66-69). */
+int ltgp_upload_population(ltgp_engine* e, uint32_t M, const uint8_t* const* ops,
+                           const uint64_t* sizes);
+
+/* Same, from one packed host buffer: genome i at buf + offsets[i]. Offsets
+   must be multiples of 16 and buf must hold ceil16(offsets[i]+sizes[i])
+   bytes; one host-to-device copy per shard (pinned buf recommended). */
+int ltgp_upload_packed(ltgp_engine* e, uint32_t M, const uint8_t* buf, uint64_t buf_bytes,
+                       const uint64_t* offsets, const uint64_t* sizes);
+
+/* evaluate_population (evolve.hpp:108-109) + evaluate_individual
+   (evolve.hpp:106): eval_batch_raw + fitness + hits + size + depth of every
+   slot. out: M records in slot order (may be NULL to keep them on device);
+   nodes: sum of sizes (may be NULL). */
+int ltgp_evaluate_population(ltgp_engine* e, ltgp_record* out, uint64_t* nodes);
+
+/* evaluate_population plus the 48 per-case outputs of every slot
+   (eval_batch_raw's result frame, eval.hpp:73-74) into outs48[M*48]. */
+int ltgp_evaluate_outputs(ltgp_engine* e, ltgp_record* out, float* outs48);
+
+/* Same work, split in two halves so callers can time the device part
+   alone: launch (async) then collect (waits, copies records). */
+int ltgp_evaluate_launch(ltgp_engine* e);
+int ltgp_evaluate_collect(ltgp_engine* e, ltgp_record* out, uint64_t* nodes);
+
+/* execute_generation (evolve.hpp:111-117): for every plan, crossover
+   (genome.hpp:80-84) mum[0,ms) ++ dad[ds,de) ++ mum[me,n) on device, then
+   evaluate the child. On success the children become the population
+   (double buffering, evolve.hpp:45). If any child would reach node_limit,
+   *size_limit_hit = 1 and the population is left unchanged. */
+int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M,
+                            ltgp_record* out, int* size_limit_hit);
+
+/* Genome bytes of slot idx (for dumps, to_text, parity). *size is always set. */
+int ltgp_download_genome(ltgp_engine* e, uint32_t idx, uint8_t* buf, uint64_t cap,
+                         uint64_t* size);
+
+/* eval_batch (eval.hpp:78-79) of one genome: the 48 per-case outputs. */
+int ltgp_eval_one(ltgp_engine* e, const uint8_t* ops, uint64_t n, float* out48);
+
+/* subtree_extent (genome.hpp:56-57) of `count` (slot, point) queries on
+   device; out holds [start, end) pairs. */
+int ltgp_subtree_extents(ltgp_engine* e, uint32_t count, const uint32_t* slots,
+                         const uint32_t* points, uint64_t* out_start_end);
+
+int ltgp_get_stats(ltgp_engine* e, ltgp_stats* out);
+uint32_t ltgp_population_size(ltgp_engine* e);
+
+/* Device address of the record array of shard s (M_s records, slots
+   [first, first + count)) and the CUDA stream it is produced on, for
+   callers that run their own collective (e.g. torch.distributed NCCL). */
+int ltgp_shard_records(ltgp_engine* e, int s, void** dev_records, uint32_t* first,
+                       uint32_t* count, void** stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,621 @@
+// ltgp_oracle.cpp — CPU ORACLE for the tree-evaluation hot path.
+//
+// TEST INFRASTRUCTURE ONLY. This file restates, in plain C++20, the
+// semantics the reference declares (headers under
+// /root/reference/proj/include/ltgp/, abbreviated H/) and specifies
+// (/root/reference/SPEC.md, abbreviated S:). It is the checker the B200
+// engine is compared against; it is never linked into the product.
+//
+// Parity status: pinned against (i) every SPEC example for the path,
+// (ii) the paper's protected-division footnote and
+// (iii) known-answer values produced by the reference's own inline code
+// (rng.hpp, eval.hpp:54-63, eval.hpp:89-98) — see tests/test_oracle.py and
+// tests/golden/. The reference ships no function bodies, so choices the
+// reference leaves open are pinned as SURVEY.md Appendix A recommends and
+// are listed next to each function.
+//
+// Build: see oracle/Makefile (-O3 -ffp-contract=off, never -ffast-math, so
+// every float op is a single IEEE round-to-nearest op, like the GPU build
+// with -fmad=false).
+
+#include "ltgp_oracle.h"
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace orc {
+
+constexpr int kLanes = 48;        // H/common.hpp:10-11
+constexpr int kConsts = 250;      // H/opcodes.hpp:18
+constexpr uint8_t kAdd = 0, kSub = 1, kMul = 2, kDiv = 3, kX = 4, kC0 = 5;  // H/opcodes.hpp:10-15
+
+inline bool is_function(uint8_t op) { return op < 4; }            // H/opcodes.hpp:22
+inline bool is_valid(uint8_t op) { return op < kC0 + kConsts; }   // H/opcodes.hpp:29
+inline int arity(uint8_t op) { return is_function(op) ? 2 : 0; }  // H/opcodes.hpp:30
+
+// H/rng.hpp:9-14
+inline uint64_t splitmix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+// H/rng.hpp:20-51: mt19937_64 seeded with splitmix64(seed); below() is the
+// debiased multiply-shift, uniform_pm1() maps the top 53 bits to [-1,1).
+struct Rng {
+    explicit Rng(uint64_t seed) : eng(splitmix64(seed)) {}
+    uint64_t below(uint64_t n) {
+        ++draws;
+        unsigned __int128 m = (unsigned __int128)eng() * n;
+        uint64_t lo = (uint64_t)m;
+        if (lo < n) {
+            uint64_t t = (0 - n) % n;
+            while (lo < t) {
+                m = (unsigned __int128)eng() * n;
+                lo = (uint64_t)m;
+            }
+        }
+        return (uint64_t)(m >> 64);
+    }
+    float uniform_pm1() {
+        ++draws;
+        double u = (double)(eng() >> 11) * 0x1.0p-53;
+        return (float)(2.0 * u - 1.0);
+    }
+    std::mt19937_64 eng;
+    uint64_t draws = 0;
+};
+
+// H/eval.hpp:54 and PAPER.md:576-578: exact-zero test, so -0.0 also gives 1.
+inline float protected_div(float a, float b) { return b != 0.0f ? a / b : 1.0f; }
+
+// H/eval.hpp:56-63
+inline float apply_op(uint8_t op, float a, float b) {
+    switch (op) {
+    case kAdd: return a + b;
+    case kSub: return a - b;
+    case kMul: return a * b;
+    default: return protected_div(a, b);
+    }
+}
+
+// H/genome.hpp:40-42: counter scan, c starts at 1, += arity-1,
+// must stay positive until the last node and reach exactly 0 there.
+bool validate(const uint8_t* ops, uint64_t n) {
+    if (n == 0) return false;
+    int64_t c = 1;
+    for (uint64_t i = 0; i < n; ++i) {
+        if (!is_valid(ops[i])) return false;
+        if (c <= 0) return false;
+        c += arity(ops[i]) - 1;
+    }
+    return c == 0;
+}
+
+// H/genome.hpp:45-46: single node has depth 1. One prefix scan with
+// a stack of "children still expected" per open function node.
+uint64_t depth(const uint8_t* ops, uint64_t n) {
+    std::vector<uint8_t> pending;  // remaining children of each open ancestor
+    uint64_t best = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        uint64_t d = pending.size() + 1;
+        best = std::max(best, d);
+        if (is_function(ops[i])) {
+            pending.push_back(2);
+        } else {
+            while (!pending.empty()) {
+                if (--pending.back() > 0) break;
+                pending.pop_back();
+            }
+        }
+    }
+    return best;
+}
+
+// H/genome.hpp:49-57: extent of the subtree rooted at idx by the
+// counter scan (need starts at 1, reaches 0 one past the subtree).
+bool subtree_extent(const uint8_t* ops, uint64_t n, uint64_t idx, uint64_t* s, uint64_t* e) {
+    if (idx >= n) return false;  // std::out_of_range in the reference
+    int64_t need = 1;
+    uint64_t i = idx;
+    while (need > 0) {
+        if (i >= n) return false;
+        need += arity(ops[i]) - 1;
+        ++i;
+    }
+    *s = idx;
+    *e = i;
+    return true;
+}
+
+// H/eval.hpp:65-68: per-case oracle, the classic recursive EVAL
+// order made iterative: a forward prefix walk with an operator stack.
+float eval_scalar(const uint8_t* ops, uint64_t n, float x, const float* consts) {
+    struct Pending { uint8_t op; bool have_left; float left; };
+    std::vector<Pending> st;
+    uint64_t pos = 0;
+    while (pos < n) {
+        uint8_t op = ops[pos++];
+        if (is_function(op)) {
+            st.push_back({op, false, 0.0f});
+            continue;
+        }
+        float v = (op == kX) ? x : consts[op - kC0];
+        while (true) {
+            if (st.empty()) return v;
+            Pending& top = st.back();
+            if (!top.have_left) {
+                top.have_left = true;
+                top.left = v;
+                break;  // evaluate the right child next
+            }
+            v = apply_op(top.op, top.left, v);
+            st.pop_back();
+        }
+    }
+    return std::nanf("");  // malformed (truncated) genome
+}
+
+// H/eval.hpp:70-79: the paper's single pass (PAPER.md:
+// 356-382): reverse scan of the prefix buffer, every node processes all 48
+// lanes before moving on; leaves push a frame, functions pop left (top) and
+// right (next) and push op(left, right). Frames are 64-byte aligned rows of
+// 48 floats (H/common.hpp:27-32). Returns the number of live frames at the
+// end (1 for a well-formed genome) or -1 on stack underflow.
+struct alignas(64) Frame { float v[kLanes]; };
+
+__attribute__((target_clones("avx512f", "avx2", "default")))
+int64_t eval_batch(const uint8_t* ops, uint64_t n, const float* inputs, const float* consts,
+                   std::vector<Frame>& stack, uint64_t* peak) {
+    int64_t top = -1;  // index of the top frame
+    uint64_t pk = 0;
+    for (uint64_t i = n; i-- > 0;) {
+        const uint8_t op = ops[i];
+        if (!is_function(op)) {
+            ++top;
+            if ((uint64_t)top >= stack.size()) stack.resize(stack.size() * 2 + 16);  // H/eval.hpp:39-40 grow
+            float* f = stack[top].v;
+            if (op == kX) {
+                for (int l = 0; l < kLanes; ++l) f[l] = inputs[l];
+            } else {
+                const float c = consts[op - kC0];
+                for (int l = 0; l < kLanes; ++l) f[l] = c;
+            }
+            if ((uint64_t)top + 1 > pk) pk = (uint64_t)top + 1;
+        } else {
+            if (top < 1) return -1;
+            float* L = stack[top].v;      // left operand = top of stack
+            float* R = stack[top - 1].v;  // right operand = next frame
+            switch (op) {
+            case kAdd: for (int l = 0; l < kLanes; ++l) R[l] = L[l] + R[l]; break;
+            case kSub: for (int l = 0; l < kLanes; ++l) R[l] = L[l] - R[l]; break;
+            case kMul: for (int l = 0; l < kLanes; ++l) R[l] = L[l] * R[l]; break;
+            default:
+                for (int l = 0; l < kLanes; ++l) R[l] = R[l] != 0.0f ? L[l] / R[l] : 1.0f;
+                break;
+            }
+            --top;
+        }
+    }
+    if (peak) *peak = pk;
+    return top + 1;
+}
+
+// H/eval.hpp:81-84: strictly sequential single
+// precision sum over lanes 0..47, then one division by 48.
+float fitness(const float* out, const float* tgt) {
+    float s = 0.0f;
+    for (int l = 0; l < kLanes; ++l) s += std::fabs(out[l] - tgt[l]);
+    return s / 48.0f;
+}
+
+// H/eval.hpp:86-87: |o - t| <= threshold (NaN is not a hit).
+int32_t hits(const float* out, const float* tgt, float thr) {
+    int32_t h = 0;
+    for (int l = 0; l < kLanes; ++l) h += (std::fabs(out[l] - tgt[l]) <= thr) ? 1 : 0;
+    return h;
+}
+
+// H/sextic.hpp:33-35: factored order, single precision.
+float target(float x) {
+    float y = x * x;
+    y = y * (x - 1.0f);
+    y = y * (x - 1.0f);
+    y = y * (x + 1.0f);
+    y = y * (x + 1.0f);
+    return y;
+}
+
+// H/sextic.hpp:37-40: 9 significant digits round-trip single precision.
+float text_round_trip(float v) {
+    char buf[64];
+    std::snprintf(buf, sizeof buf, "%.9g", (double)v);
+    return std::strtof(buf, nullptr);
+}
+
+// H/sextic.hpp:42-51. Cases first (48 uniform_pm1 draws, x and y
+// stored after the text round trip), then constants: partial Fisher-Yates
+// over the 2001 millesimal grid points with below(2001-j),
+// each parsed from its "%.3f" text, sorted ascending.
+void make_suite(Rng& rng, float* in, float* tg, float* cs) {
+    for (int l = 0; l < kLanes; ++l) {
+        float x = text_round_trip(rng.uniform_pm1());
+        in[l] = x;
+        tg[l] = text_round_trip(target(x));
+    }
+    std::vector<int> grid(2001);
+    for (int k = 0; k < 2001; ++k) grid[k] = k;
+    for (int j = 0; j < kConsts; ++j) {
+        uint64_t k = (uint64_t)j + rng.below((uint64_t)(2001 - j));
+        std::swap(grid[j], grid[k]);
+    }
+    for (int j = 0; j < kConsts; ++j) {
+        int m = grid[j] - 1000;  // thousandths in [-1000, 1000]
+        char buf[32];
+        std::snprintf(buf, sizeof buf, "%s%d.%03d", m < 0 ? "-" : "", std::abs(m) / 1000,
+                      std::abs(m) % 1000);
+        cs[j] = std::strtof(buf, nullptr);
+    }
+    std::sort(cs, cs + kConsts);
+}
+
+// suite stream decoupled from the evolution stream
+// (H/driver.hpp:17-19).
+uint64_t suite_seed(uint64_t s) { return splitmix64(s ^ 0x53554954ull); }
+
+// H/genome.hpp:59-64: prefix-order draws;
+// functions draw below(4); terminals draw 4+below(251) (X or a constant);
+// grow below the depth cap draws below(255), mapping 1:1 to opcodes.
+bool gen_node(Rng& rng, int d, int target, bool full, std::vector<uint8_t>& out, uint64_t cap) {
+    // iterative prefix construction with an explicit stack of node depths
+    std::vector<int> todo{d};
+    while (!todo.empty()) {
+        int dep = todo.back();
+        todo.pop_back();
+        uint8_t op;
+        if (dep >= target) op = (uint8_t)(4 + rng.below(251));
+        else if (full) op = (uint8_t)rng.below(4);
+        else op = (uint8_t)rng.below(255);
+        out.push_back(op);
+        if (out.size() > cap) return false;
+        if (is_function(op)) {
+            todo.push_back(dep + 1);  // right child (processed after left)
+            todo.push_back(dep + 1);  // left child
+        }
+    }
+    return true;
+}
+
+// H/genome.hpp:66-69: depth = dmin + (i/2) %
+// (dmax-dmin+1); even i -> full, odd i -> grow.
+bool ramped(Rng& rng, uint32_t count, uint64_t cap, int dmin, int dmax,
+            std::vector<std::vector<uint8_t>>& pop) {
+    pop.clear();
+    for (uint32_t i = 0; i < count; ++i) {
+        int d = dmin + (int)((i / 2) % (uint32_t)(dmax - dmin + 1));
+        bool full = (i % 2) == 0;
+        if (full && ((1ull << d) - 1) > cap) return false;  // std::length_error
+        std::vector<uint8_t> g;
+        if (!gen_node(rng, 1, d, full, g, cap)) return false;
+        pop.push_back(std::move(g));
+    }
+    return true;
+}
+
+// H/bench.hpp:13-15: exact odd size by uniform prefix
+// splits. At a function node draw the opcode (below(4)) then the left size,
+// uniform over the odd values in [1, n-2]; leaves are X or a constant with
+// equal probability (below(2)), a constant drawing 5+below(250).
+bool random_tree_of_size(Rng& rng, uint64_t n, uint8_t* out) {
+    if (n == 0 || (n % 2) == 0) return false;
+    std::vector<uint64_t> todo{n};
+    uint64_t pos = 0;
+    while (!todo.empty()) {
+        uint64_t m = todo.back();
+        todo.pop_back();
+        if (m == 1) {
+            out[pos++] = rng.below(2) == 0 ? kX : (uint8_t)(kC0 + rng.below(250));
+            continue;
+        }
+        out[pos++] = (uint8_t)rng.below(4);
+        uint64_t left = 2 * rng.below((m - 1) / 2) + 1;
+        todo.push_back(m - 1 - left);  // right, after the left subtree
+        todo.push_back(left);
+    }
+    return pos == n;
+}
+
+// H/eval.hpp:89-98
+inline bool fitness_better(float a, float b) {
+    if (std::isnan(a)) return false;
+    if (std::isnan(b)) return true;
+    return a < b;
+}
+inline bool fitness_tied(float a, float b) { return (std::isnan(a) && std::isnan(b)) || a == b; }
+
+// H/evolve.hpp:79-82: k entrants with
+// replacement, lowest wins; a tie replaces the incumbent with probability
+// 1/(ties+1) drawn from the same stream.
+uint32_t tournament(Rng& rng, uint32_t M, const float* fit, uint32_t k) {
+    uint32_t best = (uint32_t)rng.below(M);
+    uint64_t ties = 1;
+    for (uint32_t i = 1; i < k; ++i) {
+        uint32_t idx = (uint32_t)rng.below(M);
+        if (fitness_better(fit[idx], fit[best])) {
+            best = idx;
+            ties = 1;
+        } else if (fitness_tied(fit[idx], fit[best])) {
+            if (rng.below(ties + 1) == 0) best = idx;
+            ++ties;
+        }
+    }
+    return best;
+}
+
+// H/evolve.hpp:84-87: per child slot, in index order: mum
+// tournament, dad tournament, mum point, dad point. Points use the cached
+// Individual::size.
+void plan_generation(Rng& rng, uint32_t M, const float* fit, const uint32_t* size, uint32_t k,
+                     orc_plan* plans) {
+    for (uint32_t c = 0; c < M; ++c) {
+        orc_plan p;
+        p.mum_index = tournament(rng, M, fit, k);
+        p.dad_index = tournament(rng, M, fit, k);
+        p.mum_pt = (uint32_t)rng.below(size[p.mum_index]);
+        p.dad_pt = (uint32_t)rng.below(size[p.dad_index]);
+        plans[c] = p;
+    }
+}
+
+struct Suite {
+    alignas(64) float in[kLanes];
+    alignas(64) float tg[kLanes];
+    float cs[kConsts];
+};
+
+// H/evolve.hpp:106: eval + fitness + hits + size + depth of one individual.
+orc_record evaluate_individual(const uint8_t* g, uint64_t n, const Suite& s,
+                               std::vector<Frame>& stack) {
+    orc_record r;
+    alignas(64) float out[kLanes];
+    int64_t live = eval_batch(g, n, s.in, s.cs, stack, nullptr);
+    if (live != 1) {
+        r.fitness = std::nanf("");
+        r.hits = -1;
+    } else {
+        std::memcpy(out, stack[0].v, sizeof out);
+        r.fitness = fitness(out, s.tg);
+        r.hits = hits(out, s.tg, 0.01f);
+    }
+    r.size = (uint32_t)n;
+    r.depth = (uint32_t)depth(g, n);
+    return r;
+}
+
+// Dynamic pool over slots (H/evolve.hpp:108-117): which
+// worker takes which slot is decided dynamically; results land in fixed slots.
+template <class F>
+void parallel_for(uint32_t count, int threads, F&& f) {
+    if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+    std::atomic<uint32_t> next{0};
+    auto worker = [&]() {
+        std::vector<Frame> stack(64);
+        while (true) {
+            uint32_t i = next.fetch_add(1);
+            if (i >= count) break;
+            f(i, stack);
+        }
+    };
+    if (threads == 1) { worker(); return; }
+    std::vector<std::thread> ts;
+    for (int t = 0; t < threads; ++t) ts.emplace_back(worker);
+    for (auto& t : ts) t.join();
+}
+
+}  // namespace orc
+
+using namespace orc;
+
+extern "C" {
+
+uint64_t orc_splitmix64(uint64_t x) { return splitmix64(x); }
+void orc_rng_below_seq(uint64_t seed, uint64_t n, uint32_t count, uint64_t* out) {
+    Rng r(seed);
+    for (uint32_t i = 0; i < count; ++i) out[i] = r.below(n);
+}
+void orc_rng_uniform_seq(uint64_t seed, uint32_t count, float* out) {
+    Rng r(seed);
+    for (uint32_t i = 0; i < count; ++i) out[i] = r.uniform_pm1();
+}
+float orc_protected_div(float a, float b) { return protected_div(a, b); }
+int orc_fitness_better(float a, float b) { return fitness_better(a, b); }
+int orc_fitness_tied(float a, float b) { return fitness_tied(a, b); }
+// H/eval.hpp:100-102: 2*sqrt(pi*ceil(cap/2)) * safety.
+double orc_flajolet_stack_bound(uint64_t cap, double safety) {
+    return 2.0 * std::sqrt(M_PI * (double)((cap + 1) / 2)) * safety;
+}
+int orc_validate(const uint8_t* ops, uint64_t n) { return validate(ops, n); }
+uint64_t orc_depth(const uint8_t* ops, uint64_t n) { return depth(ops, n); }
+int orc_subtree_extent(const uint8_t* ops, uint64_t n, uint64_t idx, uint64_t* s, uint64_t* e) {
+    return subtree_extent(ops, n, idx, s, e) ? 0 : -1;
+}
+// H/genome.hpp:76-78: size(mum) - |extent_mum| + |extent_dad|.
+uint64_t orc_crossover_child_size(const uint8_t* mum, uint64_t mn, const uint8_t* dad, uint64_t dn,
+                                  uint64_t mp, uint64_t dp) {
+    uint64_t ms, me, ds, de;
+    if (!subtree_extent(mum, mn, mp, &ms, &me) || !subtree_extent(dad, dn, dp, &ds, &de)) return 0;
+    return mn - (me - ms) + (de - ds);
+}
+// H/genome.hpp:80-84: child = mum[0,ms) ++ dad[ds,de) ++
+// mum[me,n); size_limit_hit (nothing built) when child >= capacity.
+uint64_t orc_crossover(const uint8_t* mum, uint64_t mn, const uint8_t* dad, uint64_t dn,
+                       uint64_t mp, uint64_t dp, uint64_t cap, uint8_t* out, uint64_t out_cap,
+                       int* hit) {
+    uint64_t ms, me, ds, de;
+    *hit = 0;
+    if (!subtree_extent(mum, mn, mp, &ms, &me) || !subtree_extent(dad, dn, dp, &ds, &de)) return 0;
+    uint64_t cn = mn - (me - ms) + (de - ds);
+    if (cn >= cap) { *hit = 1; return cn; }
+    if (cn > out_cap) return 0;
+    std::memcpy(out, mum, ms);
+    std::memcpy(out + ms, dad + ds, de - ds);
+    std::memcpy(out + ms + (de - ds), mum + me, mn - me);
+    return cn;
+}
+float orc_target(float x) { return target(x); }
+uint64_t orc_suite_seed(uint64_t s) { return suite_seed(s); }
+void orc_make_suite(uint64_t seed, float* in, float* tg, float* cs) {
+    Rng r(seed);
+    make_suite(r, in, tg, cs);
+}
+uint64_t orc_gen_full(uint64_t* seed, int d, uint64_t cap, uint8_t* out, uint64_t out_cap) {
+    Rng r(*seed);
+    std::vector<uint8_t> g;
+    if (((1ull << d) - 1) > cap) return 0;
+    if (!gen_node(r, 1, d, true, g, cap) || g.size() > out_cap) return 0;
+    std::memcpy(out, g.data(), g.size());
+    return g.size();
+}
+uint64_t orc_ramped_half_and_half(uint64_t seed, uint32_t count, uint64_t cap, int dmin, int dmax,
+                                  uint8_t* out, uint64_t out_cap, uint64_t* sizes) {
+    Rng r(seed);
+    std::vector<std::vector<uint8_t>> pop;
+    if (!ramped(r, count, cap, dmin, dmax, pop)) return 0;
+    uint64_t pos = 0;
+    for (uint32_t i = 0; i < count; ++i) {
+        if (pos + pop[i].size() > out_cap) return 0;
+        std::memcpy(out + pos, pop[i].data(), pop[i].size());
+        sizes[i] = pop[i].size();
+        pos += pop[i].size();
+    }
+    return pos;
+}
+int orc_random_tree_of_size(uint64_t seed, uint64_t n, uint8_t* out) {
+    Rng r(seed);
+    return random_tree_of_size(r, n, out) ? 0 : -1;
+}
+float orc_eval_scalar(const uint8_t* ops, uint64_t n, float x, const float* cs) {
+    return eval_scalar(ops, n, x, cs);
+}
+int orc_eval_batch(const uint8_t* ops, uint64_t n, const float* in, const float* cs, float* out,
+                   uint64_t* peak) {
+    std::vector<Frame> st(64);
+    int64_t live = eval_batch(ops, n, in, cs, st, peak);
+    if (live != 1) return -1;
+    std::memcpy(out, st[0].v, sizeof(float) * kLanes);
+    return 0;
+}
+float orc_fitness(const float* o, const float* t) { return fitness(o, t); }
+int32_t orc_hits(const float* o, const float* t, float thr) { return hits(o, t, thr); }
+
+uint64_t orc_evaluate_population(uint32_t M, const uint8_t* ops, const uint64_t* off,
+                                 const uint64_t* sizes, const float* in, const float* tg,
+                                 const float* cs, int threads, orc_record* out) {
+    Suite s;
+    std::memcpy(s.in, in, sizeof s.in);
+    std::memcpy(s.tg, tg, sizeof s.tg);
+    std::memcpy(s.cs, cs, sizeof s.cs);
+    parallel_for(M, threads, [&](uint32_t i, std::vector<Frame>& st) {
+        out[i] = evaluate_individual(ops + off[i], sizes[i], s, st);
+    });
+    uint64_t nodes = 0;
+    for (uint32_t i = 0; i < M; ++i) nodes += sizes[i];
+    return nodes;
+}
+
+uint32_t orc_tournament_seq(uint64_t seed, uint32_t M, const float* fit, uint32_t k, uint32_t count,
+                            uint32_t* out) {
+    Rng r(seed);
+    for (uint32_t i = 0; i < count; ++i) out[i] = tournament(r, M, fit, k);
+    return (uint32_t)r.draws;
+}
+
+void orc_plan_generation(uint64_t seed, uint32_t M, const orc_record* pop, uint32_t k,
+                         orc_plan* out) {
+    Rng r(seed);
+    std::vector<float> fit(M);
+    std::vector<uint32_t> size(M);
+    for (uint32_t i = 0; i < M; ++i) { fit[i] = pop[i].fitness; size[i] = pop[i].size; }
+    plan_generation(r, M, fit.data(), size.data(), k, out);
+}
+
+// H/run.hpp:33-36: ramped init (depths 2..6), gen-0
+// evaluation, then plan (sequential, only RNG consumer) / execute (parallel
+// splice + evaluate into fixed child slots) until max_generations or the
+// first child reaching node_limit.
+int64_t orc_run(uint32_t M, uint32_t G, uint64_t node_limit, uint32_t k, uint64_t seed,
+                int threads, const char* dump_path, int* reason, uint64_t* nodes_evaluated) {
+    Suite s;
+    Rng srng(suite_seed(seed));
+    make_suite(srng, s.in, s.tg, s.cs);
+    Rng rng(seed);
+    std::vector<std::vector<uint8_t>> pop, next(M);
+    *reason = 0;
+    *nodes_evaluated = 0;
+    if (!ramped(rng, M, node_limit, 2, 6, pop)) return -1;
+    std::vector<orc_record> rec(M), nrec(M);
+    FILE* dump = dump_path ? std::fopen(dump_path, "w") : nullptr;
+    auto write_dump = [&](uint32_t gen) {
+        if (!dump) return;
+        // stats.hpp:104-107: fixed field order, fitness as raw bits with NaN
+        // canonicalised.
+        for (uint32_t i = 0; i < M; ++i) {
+            uint32_t bits;
+            float f = rec[i].fitness;
+            std::memcpy(&bits, &f, 4);
+            if (std::isnan(f)) bits = 0x7fc00000u;
+            std::fprintf(dump, "%u %u %u %u %d %08x\n", gen, i, rec[i].size, rec[i].depth,
+                         rec[i].hits, bits);
+        }
+    };
+    parallel_for(M, threads, [&](uint32_t i, std::vector<Frame>& st) {
+        rec[i] = evaluate_individual(pop[i].data(), pop[i].size(), s, st);
+    });
+    for (uint32_t i = 0; i < M; ++i) *nodes_evaluated += pop[i].size();
+    write_dump(0);
+    int64_t done = 0;
+    std::vector<orc_plan> plans(M);
+    std::vector<float> fit(M);
+    std::vector<uint32_t> size(M);
+    for (uint32_t gen = 1; gen <= G; ++gen) {
+        for (uint32_t i = 0; i < M; ++i) { fit[i] = rec[i].fitness; size[i] = rec[i].size; }
+        plan_generation(rng, M, fit.data(), size.data(), k, plans.data());
+        std::atomic<int> hit{0};
+        parallel_for(M, threads, [&](uint32_t c, std::vector<Frame>& st) {
+            const orc_plan& p = plans[c];
+            const auto& mum = pop[p.mum_index];
+            const auto& dad = pop[p.dad_index];
+            uint64_t ms, me, ds, de;
+            subtree_extent(mum.data(), mum.size(), p.mum_pt, &ms, &me);
+            subtree_extent(dad.data(), dad.size(), p.dad_pt, &ds, &de);
+            uint64_t cn = mum.size() - (me - ms) + (de - ds);
+            if (cn >= node_limit) { hit = 1; return; }
+            std::vector<uint8_t> child(cn);
+            std::memcpy(child.data(), mum.data(), ms);
+            std::memcpy(child.data() + ms, dad.data() + ds, de - ds);
+            std::memcpy(child.data() + ms + (de - ds), mum.data() + me, mum.size() - me);
+            nrec[c] = evaluate_individual(child.data(), cn, s, st);
+            next[c] = std::move(child);
+        });
+        if (hit) { *reason = 1; break; }
+        std::swap(pop, next);
+        std::swap(rec, nrec);
+        for (uint32_t i = 0; i < M; ++i) *nodes_evaluated += pop[i].size();
+        done = gen;
+        write_dump(gen);
+    }
+    if (dump) std::fclose(dump);
+    return done;
+}
+
+}  // extern "C"

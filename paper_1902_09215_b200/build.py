@@ -1,0 +1,78 @@
+"""In-tree build of the native libraries (no JIT cache: the .so files travel
+with the repo snapshot to the GPU box).
+
+  libltgp_cuda.so  — sm_100a kernels + the C ABI (include/ltgp_cuda.h)
+  libltgp_host.so  — C++ host API mirroring the reference (include/ltgp_host.h)
+
+The oracle (test infrastructure) is built by oracle/Makefile, see
+__graft_entry__.build().
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+HOST = os.path.join(PKG, "host")
+
+CUDA_LIB = os.path.join(PKG, "libltgp_cuda.so")
+HOST_LIB = os.path.join(PKG, "libltgp_host.so")
+
+# Bit-exactness flags: one IEEE RN op per node, no
+# FMA contraction, IEEE division, denormals preserved.
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-fmad=false", "-prec-div=true", "-prec-sqrt=true", "-ftz=false",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
+    "-Xptxas", "-v",
+]
+CXX_FLAGS = ["-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-Wall", "-pthread"]
+
+
+def _run(cmd, log=None):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if log is not None:
+        with open(log, "w") as f:
+            f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("build failed: " + " ".join(cmd))
+    return r
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _deps(dirname, exts):
+    out = []
+    for base, _, files in os.walk(dirname):
+        for f in files:
+            if f.endswith(exts):
+                out.append(os.path.join(base, f))
+    return out
+
+
+def build(force: bool = False, verbose: bool = False) -> None:
+    nvcc = os.environ.get("NVCC", "nvcc")
+    cu_deps = _deps(CSRC, (".cu", ".cuh")) + [os.path.join(ROOT, "include", "ltgp_cuda.h")]
+    if force or _stale(CUDA_LIB, cu_deps):
+        _run([nvcc, *NVCC_FLAGS, "-shared", "-o", CUDA_LIB, os.path.join(CSRC, "ltgp_engine.cu")],
+             log=os.path.join(CSRC, "ptxas.log"))
+    host_deps = _deps(HOST, (".cpp", ".hpp")) + [os.path.join(ROOT, "include", "ltgp_host.h"), CUDA_LIB]
+    if force or _stale(HOST_LIB, host_deps):
+        _run(["g++", *CXX_FLAGS, "-shared", "-o", HOST_LIB, os.path.join(HOST, "ltgp_host.cpp"),
+              "-L" + PKG, "-lltgp_cuda", "-Wl,-rpath,$ORIGIN"])
+    if verbose:
+        print("built", CUDA_LIB, HOST_LIB)
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)

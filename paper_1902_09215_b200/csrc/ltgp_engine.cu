@@ -1,0 +1,794 @@
+// ltgp_engine.cu — libltgp_cuda.so: the C ABI declared in include/ltgp_cuda.h.
+//
+// Replaces the reference's population evaluation and crossover execution
+// (/root/reference/proj/include/ltgp/evolve.hpp:106-117, genome.hpp:56-84,
+// eval.hpp:70-87) with device-resident B200 kernels. Host code here only
+// moves plans/records and orchestrates launches; every tree node is
+// evaluated on the GPU (there is no CPU fallback in this library).
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/ltgp_cuda.h"
+#include "ltgp_kernels.cuh"
+#include "ltgp_splice.cuh"
+
+using namespace ltgp_dev;
+
+namespace {
+
+constexpr int kWarps = 4;            // warps per k_eval CTA
+constexpr uint32_t kWindow = 64;     // shared stack window frames per warp
+constexpr uint32_t kDefaultChunk = 16384;
+constexpr uint32_t kMaxSteps = 1024;
+constexpr uint32_t kMaxFrames = 256;
+
+thread_local std::string g_err;
+
+void set_err(const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+}
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t _e = (call);                                                          \
+        if (_e != cudaSuccess) {                                                          \
+            set_err("%s failed: %s (%s:%d)", #call, cudaGetErrorString(_e), __FILE__, __LINE__); \
+            return -1;                                                                    \
+        }                                                                                 \
+    } while (0)
+
+#define TRY(x)                  \
+    do {                        \
+        if ((x) != 0) return -1; \
+    } while (0)
+
+// Grow-only device buffer.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    int dev = -1;
+    int ensure(size_t need, int device) {
+        if (need <= bytes && p) return 0;
+        if (p) { cudaSetDevice(dev); cudaFree(p); p = nullptr; bytes = 0; }
+        size_t nb = std::max<size_t>(need, 256);
+        nb = nb + nb / 8;  // headroom against frequent regrowth
+        cudaSetDevice(device);
+        cudaError_t e = cudaMalloc(&p, nb);
+        if (e != cudaSuccess) {
+            set_err("cudaMalloc(%zu) failed: %s", nb, cudaGetErrorString(e));
+            p = nullptr;
+            return -1;
+        }
+        bytes = nb;
+        dev = device;
+        return 0;
+    }
+    void release() {
+        if (p) { cudaSetDevice(dev); cudaFree(p); }
+        p = nullptr;
+        bytes = 0;
+    }
+    template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+struct HostBuf {  // grow-only pinned host buffer
+    void* p = nullptr;
+    size_t bytes = 0;
+    int ensure(size_t need) {
+        if (need <= bytes && p) return 0;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        size_t nb = std::max<size_t>(need, 256);
+        if (cudaMallocHost(&p, nb) != cudaSuccess) {
+            set_err("cudaMallocHost(%zu) failed", nb);
+            p = nullptr;
+            bytes = 0;
+            return -1;
+        }
+        bytes = nb;
+        return 0;
+    }
+    void release() { if (p) cudaFreeHost(p); p = nullptr; bytes = 0; }
+    template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+inline uint64_t ceil16(uint64_t x) { return (x + 15) & ~uint64_t(15); }
+
+// A set of trees resident on one device: tree i at arena + off[i].
+struct TreeSet {
+    DevBuf arena, off, size;
+    std::vector<uint64_t> h_off;
+    std::vector<uint32_t> h_size;
+    uint32_t count = 0;
+    uint64_t bytes = 0;   // used arena bytes
+    uint64_t version = 0; // bumped whenever the layout (sizes) changes
+    void release() { arena.release(); off.release(); size.release(); }
+};
+
+uint64_t g_version = 0;
+
+struct Shard {
+    int dev = 0;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev[6] = {};
+    int sms = 0;
+    int eval_grid = 0;
+    uint32_t first = 0, count = 0;  // global slot range
+    TreeSet set[2];
+    int cur = 0;
+    TreeSet scratch;                // ltgp_eval_one
+    // evaluation scratch
+    DevBuf items, ctrees, hdr, steps, frames, dframes, segs, spill, counters, rec, outs;
+    HostBuf h_items, h_ctrees, h_counters;
+    uint32_t last_items = 0, last_chunks = 0, last_ctrees = 0;
+    const TreeSet* items_for = nullptr;  // work list cache: (set, version)
+    uint64_t items_version = 0;
+    // crossover scratch
+    DevBuf plans, ext, csize, coff, dir;
+    HostBuf h_csize, h_coff, h_dir;
+    void release() {
+        set[0].release(); set[1].release(); scratch.release();
+        for (DevBuf* b : {&items, &ctrees, &hdr, &steps, &frames, &dframes, &segs, &spill, &counters,
+                          &rec, &outs, &plans, &ext, &csize, &coff, &dir}) b->release();
+        h_items.release(); h_ctrees.release(); h_counters.release();
+        h_csize.release(); h_coff.release(); h_dir.release();
+        if (st) { cudaSetDevice(dev); cudaStreamDestroy(st); }
+        for (auto& e : ev) if (e) cudaEventDestroy(e);
+    }
+};
+
+}  // namespace
+
+struct ltgp_engine {
+    ltgp_config cfg;
+    uint32_t chunk = kDefaultChunk;
+    std::vector<Shard> shards;
+    SuiteArgs suite;
+    bool have_suite = false;
+    uint32_t M = 0;
+    ltgp_stats stats;
+    HostBuf staging;
+};
+
+namespace {
+
+size_t eval_smem_bytes() { return kCtabBytes + (size_t)kWarps * (kWindow + 1) * kFrameBytes; }
+
+int init_shard(ltgp_engine* e, Shard& s) {
+    CK(cudaSetDevice(s.dev));
+    CK(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
+    for (auto& ev : s.ev) CK(cudaEventCreate(&ev));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, s.dev));
+    if (prop.major < 10) {
+        set_err("device %d is sm_%d%d; this engine is built for sm_100a (B200)", s.dev, prop.major,
+                prop.minor);
+        return -1;
+    }
+    s.sms = prop.multiProcessorCount;
+    const size_t smem = eval_smem_bytes();
+    CK(cudaFuncSetAttribute(k_eval<kWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval<kWarps>, kWarps * 32, smem));
+    if (per_sm < 1) { set_err("k_eval does not fit on an SM"); return -1; }
+    s.eval_grid = per_sm * s.sms;
+    const size_t spill_frames = e->chunk / 2 + 8;
+    TRY(s.spill.ensure((size_t)s.eval_grid * kWarps * spill_frames * kFrameBytes, s.dev));
+    TRY(s.counters.ensure(64, s.dev));
+    TRY(s.h_counters.ensure(64));
+    return 0;
+}
+
+// Evaluate every tree of `ts` on shard s: records (and optional per-case
+// outputs) land in rec/outs. Asynchronous on s.st.
+int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
+    CK(cudaSetDevice(s.dev));
+    const uint32_t C = e->chunk;
+    // --- work list (host): chunk items of large trees, then whole trees by
+    // size. Cached while the tree set's layout is unchanged.
+    if (s.items_for != &ts || s.items_version != ts.version) {
+        std::vector<Item> chunks, whole;
+        std::vector<CombineTree> ctrees;
+        uint32_t nch = 0;
+        for (uint32_t t = 0; t < ts.count; ++t) {
+            const uint32_t n = ts.h_size[t];
+            if (n <= C) {
+                whole.push_back({t, kWholeTree, 0, n});
+                continue;
+            }
+            const uint32_t k = (n + C - 1) / C;
+            ctrees.push_back({t, nch, k, n});
+            for (uint32_t j = 0; j < k; ++j) chunks.push_back({t, nch + j, j * C, std::min(n, (j + 1) * C)});
+            nch += k;
+        }
+        std::stable_sort(whole.begin(), whole.end(),
+                         [](const Item& a, const Item& b) { return a.hi > b.hi; });
+        const uint32_t nitems = (uint32_t)(chunks.size() + whole.size());
+        // the pinned staging buffers are reused: wait for older copies
+        CK(cudaStreamSynchronize(s.st));
+        TRY(s.h_items.ensure(sizeof(Item) * std::max<uint32_t>(nitems, 1)));
+        Item* hi = s.h_items.as<Item>();
+        std::copy(chunks.begin(), chunks.end(), hi);
+        std::copy(whole.begin(), whole.end(), hi + chunks.size());
+        TRY(s.items.ensure(sizeof(Item) * std::max<uint32_t>(nitems, 1), s.dev));
+        if (nitems) CK(cudaMemcpyAsync(s.items.p, hi, sizeof(Item) * nitems, cudaMemcpyHostToDevice, s.st));
+        const uint32_t nct = (uint32_t)ctrees.size();
+        if (nct) {
+            TRY(s.h_ctrees.ensure(sizeof(CombineTree) * nct));
+            std::copy(ctrees.begin(), ctrees.end(), s.h_ctrees.as<CombineTree>());
+            TRY(s.ctrees.ensure(sizeof(CombineTree) * nct, s.dev));
+            CK(cudaMemcpyAsync(s.ctrees.p, s.h_ctrees.p, sizeof(CombineTree) * nct,
+                               cudaMemcpyHostToDevice, s.st));
+            TRY(s.hdr.ensure(sizeof(ChunkHdr) * nch, s.dev));
+            TRY(s.steps.ensure((size_t)kMaxSteps * nch, s.dev));
+            TRY(s.frames.ensure((size_t)kMaxFrames * kFrameBytes * nch, s.dev));
+            TRY(s.dframes.ensure((size_t)kFrameBytes * nch, s.dev));
+            TRY(s.segs.ensure(sizeof(Seg) * 2 * nch, s.dev));
+        }
+        s.last_items = nitems;
+        s.last_chunks = nch;
+        s.last_ctrees = nct;
+        s.items_for = &ts;
+        s.items_version = ts.version;
+    }
+    const uint32_t nitems = s.last_items, nch = s.last_chunks, nct = s.last_ctrees;
+    (void)nch;
+    TRY(s.rec.ensure(sizeof(ltgp_record) * std::max<uint32_t>(ts.count, 1), s.dev));
+    if (want_outs) TRY(s.outs.ensure(sizeof(float) * kLanes * std::max<uint32_t>(ts.count, 1), s.dev));
+    CK(cudaMemsetAsync(s.counters.p, 0, 64, s.st));
+    EvalArgs a;
+    a.arena = ts.arena.as<uint8_t>();
+    a.off = ts.off.as<uint64_t>();
+    a.size = ts.size.as<uint32_t>();
+    a.items = s.items.as<Item>();
+    a.n_items = nitems;
+    a.counters = s.counters.as<uint32_t>();
+    a.hdr = s.hdr.as<ChunkHdr>();
+    a.steps = s.steps.as<uint8_t>();
+    a.frames = s.frames.as<float2>();
+    a.max_steps = kMaxSteps;
+    a.max_frames = kMaxFrames;
+    a.spill = s.spill.as<float2>();
+    a.spill_frames = C / 2 + 8;
+    a.rec = s.rec.as<float>();
+    a.outs = want_outs ? s.outs.as<float>() : nullptr;
+    a.stack_frames = kWindow;
+    CK(cudaEventRecord(s.ev[0], s.st));
+    uint32_t launches = 0;
+    if (nitems) {
+        const int grid = std::min<int>(s.eval_grid, (int)nitems);
+        k_eval<kWarps><<<std::max(grid, 1), kWarps * 32, eval_smem_bytes(), s.st>>>(a, e->suite);
+        CK(cudaGetLastError());
+        ++launches;
+    }
+    CK(cudaEventRecord(s.ev[4], s.st));
+    if (nct) {
+        CombineArgs ca;
+        ca.trees = s.ctrees.as<CombineTree>();
+        ca.n_trees = nct;
+        ca.hdr = s.hdr.as<ChunkHdr>();
+        ca.steps = s.steps.as<uint8_t>();
+        ca.frames = s.frames.as<float2>();
+        ca.max_steps = kMaxSteps;
+        ca.max_frames = kMaxFrames;
+        ca.dframes = s.dframes.as<float2>();
+        ca.segs = s.segs.as<Seg>();
+        ca.rec = s.rec.as<float>();
+        ca.outs = a.outs;
+        ca.counters = s.counters.as<uint32_t>();
+        const int blocks = (int)std::min<uint32_t>((nct + 3) / 4, (uint32_t)s.sms * 16);
+        k_combine<<<blocks, 128, 0, s.st>>>(ca, e->suite);
+        CK(cudaGetLastError());
+        ++launches;
+    }
+    CK(cudaEventRecord(s.ev[1], s.st));
+    CK(cudaMemcpyAsync(s.h_counters.p, s.counters.p, 64, cudaMemcpyDeviceToHost, s.st));
+    e->stats.kernel_launches = launches;
+    return 0;
+}
+
+int check_eval(Shard& s) {
+    const uint32_t* c = s.h_counters.as<uint32_t>();
+    if (c[1] & 2u) { set_err("malformed genome (stack underflow or leftover values)"); return -1; }
+    if (c[2] != 0 || (c[1] & 1u)) {
+        set_err("chunk summary overflow in %u chunks (raise chunk capacity)", c[2]);
+        return -1;
+    }
+    return 0;
+}
+
+// Assign contiguous slot ranges to shards, balanced by bytes.
+void partition(ltgp_engine* e, uint32_t M, const uint64_t* sizes) {
+    const int G = (int)e->shards.size();
+    uint64_t total = 0;
+    for (uint32_t i = 0; i < M; ++i) total += sizes ? sizes[i] : 1;
+    uint32_t i = 0;
+    uint64_t acc = 0;
+    for (int g = 0; g < G; ++g) {
+        Shard& s = e->shards[g];
+        s.first = i;
+        const uint64_t goal = (total * (uint64_t)(g + 1)) / (uint64_t)G;
+        while (i < M && (g == G - 1 || acc + (sizes ? sizes[i] : 1) / 2 < goal)) {
+            acc += sizes ? sizes[i] : 1;
+            ++i;
+        }
+        s.count = i - s.first;
+    }
+}
+
+int set_layout(Shard& s, TreeSet& ts, uint32_t count, const uint64_t* sizes, uint64_t* offs_out) {
+    bool same = ts.count == count && ts.h_size.size() == count && ts.version != 0;
+    for (uint32_t i = 0; same && i < count; ++i) same = ts.h_size[i] == sizes[i];
+    if (!same) ts.version = ++g_version;
+    ts.count = count;
+    ts.h_off.resize(count);
+    ts.h_size.resize(count);
+    uint64_t o = 0;
+    for (uint32_t i = 0; i < count; ++i) {
+        if (sizes[i] == 0 || sizes[i] > 0xffffffffull) {
+            set_err("genome size %llu out of range", (unsigned long long)sizes[i]);
+            return -1;
+        }
+        ts.h_off[i] = o;
+        ts.h_size[i] = (uint32_t)sizes[i];
+        if (offs_out) offs_out[i] = o;
+        o += ceil16(sizes[i]);
+    }
+    ts.bytes = o;
+    TRY(ts.arena.ensure(std::max<uint64_t>(o, 16) + 64, s.dev));
+    TRY(ts.off.ensure(sizeof(uint64_t) * std::max<uint32_t>(count, 1), s.dev));
+    TRY(ts.size.ensure(sizeof(uint32_t) * std::max<uint32_t>(count, 1), s.dev));
+    return 0;
+}
+
+int upload_tables(Shard& s, TreeSet& ts) {
+    CK(cudaSetDevice(s.dev));
+    if (ts.count == 0) return 0;
+    CK(cudaMemcpyAsync(ts.off.p, ts.h_off.data(), sizeof(uint64_t) * ts.count, cudaMemcpyHostToDevice, s.st));
+    CK(cudaMemcpyAsync(ts.size.p, ts.h_size.data(), sizeof(uint32_t) * ts.count, cudaMemcpyHostToDevice, s.st));
+    CK(cudaStreamSynchronize(s.st));  // host vectors may change after return
+    return 0;
+}
+
+int collect(ltgp_engine* e, ltgp_record* out, float* outs48) {
+    double secs = 0.0, ksecs = 0.0, csecs = 0.0;
+    uint64_t nodes = 0, chunks = 0;
+    for (Shard& s : e->shards) {
+        CK(cudaSetDevice(s.dev));
+        if (out && s.count) CK(cudaMemcpyAsync(out + s.first, s.rec.p, sizeof(ltgp_record) * s.count,
+                                               cudaMemcpyDeviceToHost, s.st));
+        if (outs48 && s.count) CK(cudaMemcpyAsync(outs48 + (size_t)s.first * kLanes, s.outs.p,
+                                                  sizeof(float) * kLanes * s.count,
+                                                  cudaMemcpyDeviceToHost, s.st));
+        CK(cudaStreamSynchronize(s.st));
+        TRY(check_eval(s));
+        float ms = 0.0f;
+        CK(cudaEventElapsedTime(&ms, s.ev[0], s.ev[1]));
+        secs = std::max(secs, ms * 1e-3);
+        CK(cudaEventElapsedTime(&ms, s.ev[0], s.ev[4]));
+        ksecs = std::max(ksecs, ms * 1e-3);
+        CK(cudaEventElapsedTime(&ms, s.ev[4], s.ev[1]));
+        csecs = std::max(csecs, ms * 1e-3);
+        const TreeSet& ts = s.set[s.cur];
+        for (uint32_t i = 0; i < ts.count; ++i) nodes += ts.h_size[i];
+        chunks += s.last_chunks;
+    }
+    e->stats.eval_seconds = secs;
+    e->stats.eval_kernel_seconds = ksecs;
+    e->stats.combine_seconds = csecs;
+    e->stats.nodes_evaluated += nodes;
+    e->stats.last_chunks = chunks;
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ltgp_last_error(void) { return g_err.c_str(); }
+const char* ltgp_version(void) { return "ltgp_cuda 0.1 (sm_100a)"; }
+
+int ltgp_engine_create(const ltgp_config* cfg, ltgp_engine** out) {
+    if (!cfg || !out) { set_err("null argument"); return -1; }
+    if (cfg->n_shards < 1 || cfg->n_shards > LTGP_MAX_SHARDS) { set_err("n_shards out of range"); return -1; }
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    for (int i = 0; i < cfg->n_shards; ++i)
+        if (cfg->devices[i] < 0 || cfg->devices[i] >= ndev) {
+            set_err("device %d not present (%d visible)", cfg->devices[i], ndev);
+            return -1;
+        }
+    auto e = std::make_unique<ltgp_engine>();
+    e->cfg = *cfg;
+    if (cfg->chunk_nodes) {
+        if (cfg->chunk_nodes % 16 || cfg->chunk_nodes < 64) { set_err("chunk_nodes must be a multiple of 16 >= 64"); return -1; }
+        e->chunk = cfg->chunk_nodes;
+    }
+    std::memset(&e->stats, 0, sizeof e->stats);
+    e->shards.resize(cfg->n_shards);
+    for (int i = 0; i < cfg->n_shards; ++i) {
+        e->shards[i].dev = cfg->devices[i];
+        if (init_shard(e.get(), e->shards[i]) != 0) {
+            for (auto& s : e->shards) s.release();
+            return -1;
+        }
+    }
+    // peer access between distinct devices (parents are read over NVLink)
+    for (int i = 0; i < cfg->n_shards; ++i)
+        for (int j = 0; j < cfg->n_shards; ++j) {
+            const int a = cfg->devices[i], b = cfg->devices[j];
+            if (a == b) continue;
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, a, b);
+            if (!can) { set_err("no peer access %d -> %d", a, b); return -1; }
+            cudaSetDevice(a);
+            cudaError_t pe = cudaDeviceEnablePeerAccess(b, 0);
+            if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) {
+                set_err("cudaDeviceEnablePeerAccess(%d->%d): %s", a, b, cudaGetErrorString(pe));
+                return -1;
+            }
+            cudaGetLastError();
+        }
+    *out = e.release();
+    return 0;
+}
+
+int ltgp_engine_destroy(ltgp_engine* e) {
+    if (!e) return 0;
+    for (auto& s : e->shards) {
+        cudaSetDevice(s.dev);
+        if (s.st) cudaStreamSynchronize(s.st);
+        s.release();
+    }
+    e->staging.release();
+    delete e;
+    return 0;
+}
+
+int ltgp_set_suite(ltgp_engine* e, const float* in, const float* tg, const float* cs) {
+    if (!e || !in || !tg || !cs) { set_err("null argument"); return -1; }
+    for (int l = 0; l < 24; ++l) {
+        e->suite.x[l] = make_float2(in[2 * l], in[2 * l + 1]);
+        e->suite.t[l] = make_float2(tg[2 * l], tg[2 * l + 1]);
+    }
+    for (int i = 0; i < 256; ++i) e->suite.c[i] = (i >= 5 && i < 255) ? cs[i - 5] : 0.0f;
+    e->have_suite = true;
+    return 0;
+}
+
+int ltgp_upload_packed(ltgp_engine* e, uint32_t M, const uint8_t* buf, uint64_t buf_bytes,
+                       const uint64_t* offsets, const uint64_t* sizes) {
+    if (!e || (M && (!buf || !offsets || !sizes))) { set_err("null argument"); return -1; }
+    for (uint32_t i = 0; i < M; ++i) {
+        if (offsets[i] % 16) { set_err("offset of genome %u not 16-aligned", i); return -1; }
+        if (i && offsets[i] < offsets[i - 1] + sizes[i - 1]) { set_err("offsets not increasing/overlapping at %u", i); return -1; }
+        if (offsets[i] + sizes[i] > buf_bytes) {
+            set_err("genome %u exceeds buffer", i);
+            return -1;
+        }
+    }
+    partition(e, M, sizes);
+    for (Shard& s : e->shards) {
+        s.cur = 0;
+        TreeSet& ts = s.set[0];
+        if (s.count == 0) { ts.count = 0; continue; }
+        const uint64_t base = offsets[s.first];
+        std::vector<uint64_t> rel(s.count);
+        TRY(set_layout(s, ts, s.count, sizes + s.first, nullptr));
+        for (uint32_t i = 0; i < s.count; ++i) ts.h_off[i] = offsets[s.first + i] - base;
+        const uint64_t last = s.first + s.count - 1;
+        const uint64_t span = std::min<uint64_t>(ceil16(offsets[last] + sizes[last]), buf_bytes) - base;
+        TRY(ts.arena.ensure(span + 64, s.dev));
+        ts.bytes = span;
+        CK(cudaSetDevice(s.dev));
+        CK(cudaMemcpyAsync(ts.arena.p, buf + base, span, cudaMemcpyHostToDevice, s.st));
+        TRY(upload_tables(s, ts));
+    }
+    e->M = M;
+    return 0;
+}
+
+int ltgp_upload_population(ltgp_engine* e, uint32_t M, const uint8_t* const* ops,
+                           const uint64_t* sizes) {
+    if (!e || (M && (!ops || !sizes))) { set_err("null argument"); return -1; }
+    partition(e, M, sizes);
+    for (Shard& s : e->shards) {
+        s.cur = 0;
+        TreeSet& ts = s.set[0];
+        if (s.count == 0) { ts.count = 0; continue; }
+        TRY(set_layout(s, ts, s.count, sizes + s.first, nullptr));
+        CK(cudaSetDevice(s.dev));
+        CK(cudaStreamSynchronize(s.st));
+        TRY(e->staging.ensure(ts.bytes + 16));
+        uint8_t* h = e->staging.as<uint8_t>();
+        for (uint32_t i = 0; i < s.count; ++i) {
+            std::memcpy(h + ts.h_off[i], ops[s.first + i], sizes[s.first + i]);
+            const uint64_t pad = ceil16(sizes[s.first + i]) - sizes[s.first + i];
+            if (pad) std::memset(h + ts.h_off[i] + sizes[s.first + i], 0xff, pad);
+        }
+        CK(cudaMemcpyAsync(ts.arena.p, h, ts.bytes, cudaMemcpyHostToDevice, s.st));
+        TRY(upload_tables(s, ts));  // synchronizes: staging reusable
+    }
+    e->M = M;
+    return 0;
+}
+
+int ltgp_evaluate_launch(ltgp_engine* e) {
+    if (!e) { set_err("null engine"); return -1; }
+    if (!e->have_suite) { set_err("ltgp_set_suite not called"); return -1; }
+    for (Shard& s : e->shards)
+        if (s.count) TRY(launch_eval(e, s, s.set[s.cur], false));
+    return 0;
+}
+
+int ltgp_evaluate_collect(ltgp_engine* e, ltgp_record* out, uint64_t* nodes) {
+    if (!e) { set_err("null engine"); return -1; }
+    const uint64_t before = e->stats.nodes_evaluated;
+    TRY(collect(e, out, nullptr));
+    if (nodes) *nodes = e->stats.nodes_evaluated - before;
+    return 0;
+}
+
+int ltgp_evaluate_population(ltgp_engine* e, ltgp_record* out, uint64_t* nodes) {
+    TRY(ltgp_evaluate_launch(e));
+    return ltgp_evaluate_collect(e, out, nodes);
+}
+
+int ltgp_evaluate_outputs(ltgp_engine* e, ltgp_record* out, float* outs48) {
+    if (!e) { set_err("null engine"); return -1; }
+    if (!e->have_suite) { set_err("ltgp_set_suite not called"); return -1; }
+    for (Shard& s : e->shards)
+        if (s.count) TRY(launch_eval(e, s, s.set[s.cur], true));
+    return collect(e, out, outs48);
+}
+
+int ltgp_eval_one(ltgp_engine* e, const uint8_t* ops, uint64_t n, float* out48) {
+    if (!e || !ops || !out48) { set_err("null argument"); return -1; }
+    if (!e->have_suite) { set_err("ltgp_set_suite not called"); return -1; }
+    Shard& s = e->shards[0];
+    TreeSet& ts = s.scratch;
+    uint64_t sz = n;
+    TRY(set_layout(s, ts, 1, &sz, nullptr));
+    CK(cudaSetDevice(s.dev));
+    CK(cudaStreamSynchronize(s.st));
+    TRY(e->staging.ensure(ceil16(n) + 16));
+    uint8_t* h = e->staging.as<uint8_t>();
+    std::memcpy(h, ops, n);
+    std::memset(h + n, 0xff, ceil16(n) - n);
+    CK(cudaMemcpyAsync(ts.arena.p, h, ceil16(n), cudaMemcpyHostToDevice, s.st));
+    TRY(upload_tables(s, ts));
+    TRY(launch_eval(e, s, ts, true));
+    CK(cudaMemcpyAsync(out48, s.outs.p, sizeof(float) * kLanes, cudaMemcpyDeviceToHost, s.st));
+    CK(cudaStreamSynchronize(s.st));
+    return check_eval(s);
+}
+
+int ltgp_get_stats(ltgp_engine* e, ltgp_stats* out) {
+    if (!e || !out) { set_err("null argument"); return -1; }
+    uint64_t hw = 0;
+    for (Shard& s : e->shards)
+        for (auto& ts : s.set) hw = std::max<uint64_t>(hw, ts.arena.bytes);
+    e->stats.arena_high_water = hw;
+    *out = e->stats;
+    return 0;
+}
+
+uint32_t ltgp_population_size(ltgp_engine* e) { return e ? e->M : 0; }
+
+int ltgp_shard_records(ltgp_engine* e, int s, void** dev_records, uint32_t* first, uint32_t* count,
+                       void** stream) {
+    if (!e || s < 0 || s >= (int)e->shards.size()) { set_err("bad shard"); return -1; }
+    Shard& sh = e->shards[s];
+    if (dev_records) *dev_records = sh.rec.p;
+    if (first) *first = sh.first;
+    if (count) *count = sh.count;
+    if (stream) *stream = (void*)sh.st;
+    return 0;
+}
+
+int ltgp_download_genome(ltgp_engine* e, uint32_t idx, uint8_t* buf, uint64_t cap, uint64_t* size) {
+    if (!e || !size) { set_err("null argument"); return -1; }
+    for (Shard& s : e->shards) {
+        if (idx < s.first || idx >= s.first + s.count) continue;
+        const TreeSet& ts = s.set[s.cur];
+        const uint32_t i = idx - s.first;
+        *size = ts.h_size[i];
+        if (!buf || cap < ts.h_size[i]) return 0;
+        CK(cudaSetDevice(s.dev));
+        CK(cudaMemcpyAsync(buf, ts.arena.as<uint8_t>() + ts.h_off[i], ts.h_size[i],
+                           cudaMemcpyDeviceToHost, s.st));
+        CK(cudaStreamSynchronize(s.st));
+        return 0;
+    }
+    set_err("slot %u out of range (M=%u)", idx, e->M);
+    return -1;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Crossover on device: execute_generation (evolve.hpp:111-117).
+// ---------------------------------------------------------------------------
+namespace {
+
+// Directory of the current population: per global slot, its device address
+// and size (parents may be read from any shard's GPU).
+int build_directory(ltgp_engine* e, std::vector<DirEntry>& dir) {
+    dir.assign(e->M, DirEntry{nullptr, 0});
+    for (Shard& s : e->shards) {
+        const TreeSet& ts = s.set[s.cur];
+        for (uint32_t i = 0; i < s.count; ++i)
+            dir[s.first + i] = DirEntry{ts.arena.as<uint8_t>() + ts.h_off[i], ts.h_size[i]};
+    }
+    return 0;
+}
+
+int upload_directory(ltgp_engine* e, Shard& s, const std::vector<DirEntry>& dir) {
+    CK(cudaSetDevice(s.dev));
+    TRY(s.dir.ensure(sizeof(DirEntry) * std::max<size_t>(dir.size(), 1), s.dev));
+    TRY(s.h_dir.ensure(sizeof(DirEntry) * std::max<size_t>(dir.size(), 1)));
+    CK(cudaStreamSynchronize(s.st));
+    std::memcpy(s.h_dir.p, dir.data(), sizeof(DirEntry) * dir.size());
+    CK(cudaMemcpyAsync(s.dir.p, s.h_dir.p, sizeof(DirEntry) * dir.size(), cudaMemcpyHostToDevice, s.st));
+    (void)e;
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M, ltgp_record* out,
+                            int* size_limit_hit) {
+    if (!e || !plans || !size_limit_hit) { set_err("null argument"); return -1; }
+    if (M != e->M) { set_err("plan count %u != population size %u", M, e->M); return -1; }
+    if (!e->have_suite) { set_err("ltgp_set_suite not called"); return -1; }
+    *size_limit_hit = 0;
+    for (uint32_t c = 0; c < M; ++c)
+        if (plans[c].mum_index >= M || plans[c].dad_index >= M) {
+            set_err("plan %u references slot outside the population", c);
+            return -1;
+        }
+    std::vector<DirEntry> dir;
+    build_directory(e, dir);
+    for (uint32_t c = 0; c < M; ++c)
+        if (plans[c].mum_pt >= dir[plans[c].mum_index].size || plans[c].dad_pt >= dir[plans[c].dad_index].size) {
+            set_err("plan %u: crossover point out of range", c);  // std::out_of_range
+            return -1;
+        }
+    // 1. extents for children in equal-count ranges
+    const int G = (int)e->shards.size();
+    std::vector<uint32_t> qfirst(G), qcount(G);
+    for (int g = 0; g < G; ++g) {
+        qfirst[g] = (uint32_t)((uint64_t)M * g / G);
+        qcount[g] = (uint32_t)((uint64_t)M * (g + 1) / G) - qfirst[g];
+    }
+    std::vector<Extent> ext(M);
+    std::vector<uint64_t> csize(M);
+    for (int g = 0; g < G; ++g) {
+        Shard& s = e->shards[g];
+        TRY(upload_directory(e, s, dir));
+        if (!qcount[g]) continue;
+        TRY(s.plans.ensure(sizeof(PlanDev) * M, s.dev));
+        TRY(s.ext.ensure(sizeof(Extent) * M, s.dev));
+        TRY(s.csize.ensure(sizeof(uint64_t) * M, s.dev));
+        CK(cudaMemcpyAsync(s.plans.p, plans + qfirst[g], sizeof(PlanDev) * qcount[g], cudaMemcpyHostToDevice, s.st));
+        CK(cudaMemsetAsync(s.counters.p, 0, 64, s.st));
+        CK(cudaEventRecord(s.ev[2], s.st));
+        const uint32_t warps = 2 * qcount[g];
+        k_extent<<<(warps + 3) / 4, 128, 0, s.st>>>(s.plans.as<PlanDev>(), qcount[g], s.dir.as<DirEntry>(),
+                                                  s.ext.as<Extent>(), nullptr, s.counters.as<uint32_t>() + 3);
+        CK(cudaGetLastError());
+        k_child_size<<<(qcount[g] + 127) / 128, 128, 0, s.st>>>(s.plans.as<PlanDev>(), qcount[g],
+                                                              s.dir.as<DirEntry>(), s.ext.as<Extent>(),
+                                                              s.csize.as<uint64_t>());
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(ext.data() + qfirst[g], s.ext.p, sizeof(Extent) * qcount[g], cudaMemcpyDeviceToHost, s.st));
+        CK(cudaMemcpyAsync(csize.data() + qfirst[g], s.csize.p, sizeof(uint64_t) * qcount[g], cudaMemcpyDeviceToHost, s.st));
+        CK(cudaMemcpyAsync(s.h_counters.p, s.counters.p, 64, cudaMemcpyDeviceToHost, s.st));
+    }
+    for (int g = 0; g < G; ++g) {
+        Shard& s = e->shards[g];
+        CK(cudaSetDevice(s.dev));
+        CK(cudaStreamSynchronize(s.st));
+        if (qcount[g] && s.h_counters.as<uint32_t>()[3]) { set_err("malformed parent genome in extent scan"); return -1; }
+    }
+    // 2. SizeLimitHit (genome.hpp:71-84): child >= node_limit
+    for (uint32_t c = 0; c < M; ++c)
+        if (csize[c] >= e->cfg.node_limit || csize[c] > 0xffffffffull) { *size_limit_hit = 1; return 0; }
+    // 3. children partitioned by bytes; splice into the other buffer
+    // (parents stay readable until every shard has spliced).
+    std::vector<uint32_t> old_cur(G);
+    for (int g = 0; g < G; ++g) old_cur[g] = e->shards[g].cur;
+    partition(e, M, csize.data());
+    float splice_ms = 0.0f;
+    for (int g = 0; g < G; ++g) {
+        Shard& s = e->shards[g];
+        TreeSet& ts = s.set[1 - s.cur];
+        if (s.count == 0) { ts.count = 0; continue; }
+        std::vector<uint64_t> coff(s.count);
+        TRY(set_layout(s, ts, s.count, csize.data() + s.first, coff.data()));
+        CK(cudaSetDevice(s.dev));
+        TRY(s.coff.ensure(sizeof(uint64_t) * s.count, s.dev));
+        TRY(s.h_coff.ensure(sizeof(uint64_t) * s.count * 2 + sizeof(Extent) * s.count + sizeof(PlanDev) * s.count));
+        uint8_t* hb = s.h_coff.as<uint8_t>();
+        std::memcpy(hb, coff.data(), sizeof(uint64_t) * s.count);
+        std::memcpy(hb + 8 * s.count, csize.data() + s.first, sizeof(uint64_t) * s.count);
+        std::memcpy(hb + 16 * s.count, ext.data() + s.first, sizeof(Extent) * s.count);
+        std::memcpy(hb + 32 * s.count, plans + s.first, sizeof(PlanDev) * s.count);
+        CK(cudaMemcpyAsync(s.coff.p, hb, 8 * s.count, cudaMemcpyHostToDevice, s.st));
+        CK(cudaMemcpyAsync(s.csize.p, hb + 8 * s.count, 8 * s.count, cudaMemcpyHostToDevice, s.st));
+        CK(cudaMemcpyAsync(s.ext.p, hb + 16 * s.count, sizeof(Extent) * s.count, cudaMemcpyHostToDevice, s.st));
+        CK(cudaMemcpyAsync(s.plans.p, hb + 32 * s.count, sizeof(PlanDev) * s.count, cudaMemcpyHostToDevice, s.st));
+        CK(cudaEventRecord(s.ev[2], s.st));
+        k_splice<<<std::min<uint32_t>(s.count, (uint32_t)s.sms * 8), 256, 0, s.st>>>(
+            s.plans.as<PlanDev>(), s.count, s.dir.as<DirEntry>(), s.ext.as<Extent>(), s.coff.as<uint64_t>(),
+            s.csize.as<uint64_t>(), ts.arena.as<uint8_t>());
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(s.ev[3], s.st));
+        CK(cudaMemcpyAsync(ts.off.p, ts.h_off.data(), sizeof(uint64_t) * ts.count, cudaMemcpyHostToDevice, s.st));
+        CK(cudaMemcpyAsync(ts.size.p, ts.h_size.data(), sizeof(uint32_t) * ts.count, cudaMemcpyHostToDevice, s.st));
+    }
+    for (int g = 0; g < G; ++g) {
+        Shard& s = e->shards[g];
+        CK(cudaSetDevice(s.dev));
+        CK(cudaStreamSynchronize(s.st));  // all splices done: parents may be dropped
+        if (s.count) {
+            float ms = 0.0f;
+            CK(cudaEventElapsedTime(&ms, s.ev[2], s.ev[3]));
+            splice_ms = std::max(splice_ms, ms);
+        }
+    }
+    for (int g = 0; g < G; ++g) e->shards[g].cur = 1 - old_cur[g];
+    e->stats.splice_seconds = splice_ms * 1e-3;
+    // 4. evaluate the children
+    TRY(ltgp_evaluate_launch(e));
+    return ltgp_evaluate_collect(e, out, nullptr);
+}
+
+int ltgp_subtree_extents(ltgp_engine* e, uint32_t count, const uint32_t* slots, const uint32_t* points,
+                         uint64_t* out) {
+    if (!e || (count && (!slots || !points || !out))) { set_err("null argument"); return -1; }
+    std::vector<DirEntry> dir;
+    build_directory(e, dir);
+    std::vector<PlanDev> q(count);
+    for (uint32_t i = 0; i < count; ++i) {
+        if (slots[i] >= e->M) { set_err("slot out of range"); return -1; }
+        if (points[i] >= dir[slots[i]].size) { set_err("point out of range"); return -1; }
+        q[i] = PlanDev{slots[i], slots[i], points[i], points[i]};
+    }
+    Shard& s = e->shards[0];
+    TRY(upload_directory(e, s, dir));
+    TRY(s.plans.ensure(sizeof(PlanDev) * std::max<uint32_t>(count, 1), s.dev));
+    TRY(s.ext.ensure(sizeof(Extent) * std::max<uint32_t>(count, 1), s.dev));
+    CK(cudaMemcpyAsync(s.plans.p, q.data(), sizeof(PlanDev) * count, cudaMemcpyHostToDevice, s.st));
+    CK(cudaMemsetAsync(s.counters.p, 0, 64, s.st));
+    if (count) {
+        k_extent<<<(2 * count + 3) / 4, 128, 0, s.st>>>(s.plans.as<PlanDev>(), count, s.dir.as<DirEntry>(),
+                                                        s.ext.as<Extent>(), nullptr, s.counters.as<uint32_t>() + 3);
+        CK(cudaGetLastError());
+    }
+    std::vector<Extent> ext(count);
+    CK(cudaMemcpyAsync(ext.data(), s.ext.p, sizeof(Extent) * count, cudaMemcpyDeviceToHost, s.st));
+    CK(cudaMemcpyAsync(s.h_counters.p, s.counters.p, 64, cudaMemcpyDeviceToHost, s.st));
+    CK(cudaStreamSynchronize(s.st));
+    if (s.h_counters.as<uint32_t>()[3]) { set_err("malformed genome in extent scan"); return -1; }
+    for (uint32_t i = 0; i < count; ++i) { out[2 * i] = ext[i].ms; out[2 * i + 1] = ext[i].me; }
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,165 @@
+// ltgp_splice.cuh — device-side subtree crossover.
+//
+// k_extent replaces subtree_extent (/root/reference/proj/include/ltgp/
+// genome.hpp:49-57): counter scan from the crossover point until the need
+// count reaches zero, one warp per query, 512 opcode bytes per step.
+// k_splice replaces crossover (genome.hpp:80-84):
+// child = mum[0,ms) ++ dad[ds,de) ++ mum[me,n), one CTA per child, written as
+// aligned 32-bit words assembled with funnel shifts from the (unaligned)
+// parent bytes, which may live on a peer GPU (read over NVLink by UVA).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ltgp_dev {
+
+struct DirEntry {          // one population slot
+    const uint8_t* ptr;    // device address of the genome (any GPU, UVA)
+    uint64_t size;
+};
+
+struct PlanDev {
+    uint32_t mum, dad, mum_pt, dad_pt;
+};
+
+struct Extent {            // per child: mum [ms, me), dad [ds, de)
+    uint32_t ms, me, ds, de;
+};
+
+// One warp per query q: child q/2, parent = mum (q even) or dad (q odd).
+__global__ void __launch_bounds__(128) k_extent(const PlanDev* plans, uint32_t count,
+                                                const DirEntry* dir, Extent* ext,
+                                                uint64_t* child_size, uint32_t* err) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (q >= 2 * count) return;
+    const uint32_t c = q >> 1;
+    const bool is_dad = q & 1;
+    const PlanDev p = plans[c];
+    const DirEntry d = dir[is_dad ? p.dad : p.mum];
+    const uint64_t pt = is_dad ? p.dad_pt : p.mum_pt;
+    const uint64_t n = d.size;
+    if (pt >= n) {  // std::out_of_range in the reference
+        if (lane == 0) atomicOr(err, 4u);
+        return;
+    }
+    int64_t need = 1;  // children still expected when reaching byte pos
+    uint64_t base = pt & ~uint64_t(15);
+    uint64_t end = 0;
+    bool found = false;
+    while (!found && base < n) {
+        const uint64_t lb = base + 16ull * lane;  // this lane's 16 bytes
+        int delta[16];
+        int tot = 0;
+        if (lb < n) {
+            const uint4 w = *reinterpret_cast<const uint4*>(d.ptr + lb);
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const uint64_t pos = lb + k;
+                const uint32_t b = (ws[k >> 2] >> (8 * (k & 3))) & 0xffu;
+                const int dk = (pos < pt || pos >= n) ? 0 : (b < 4u ? 1 : -1);
+                delta[k] = dk;
+                tot += dk;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) delta[k] = 0;
+        }
+        // exclusive warp scan of lane totals
+        int incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if ((int)lane >= o) incl += v;
+        }
+        int run = (int)need + incl - tot;
+        int hit = -1;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            run += delta[k];
+            if (hit < 0 && delta[k] != 0 && run == 0) hit = k;
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, hit >= 0);
+        if (m) {
+            const int src = __ffs(m) - 1;
+            const int h = __shfl_sync(0xffffffffu, hit, src);
+            end = base + 16ull * src + (uint64_t)h + 1;
+            found = true;
+        } else {
+            need += __shfl_sync(0xffffffffu, incl, 31);
+            base += 512;
+        }
+    }
+    if (!found) {
+        if (lane == 0) atomicOr(err, 2u);
+        return;
+    }
+    if (lane == 0) {
+        if (is_dad) { ext[c].ds = (uint32_t)pt; ext[c].de = (uint32_t)end; }
+        else { ext[c].ms = (uint32_t)pt; ext[c].me = (uint32_t)end; }
+    }
+}
+
+// child size from both extents (crossover_child_size, genome.hpp:76-78)
+__global__ void k_child_size(const PlanDev* plans, uint32_t count, const DirEntry* dir,
+                             const Extent* ext, uint64_t* child_size) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= count) return;
+    const Extent x = ext[c];
+    const uint64_t mn = dir[plans[c].mum].size;
+    child_size[c] = mn - (uint64_t)(x.me - x.ms) + (uint64_t)(x.de - x.ds);
+}
+
+__device__ __forceinline__ uint32_t ld_word_unaligned(const uint8_t* p) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+    const uint32_t sh = (uint32_t)(a & 3) * 8;
+    const uint32_t lo = w[0];
+    if (sh == 0) return lo;
+    return __funnelshift_r(lo, w[1], sh);
+}
+
+// One CTA per child; dst offsets are 16-aligned, bytes past the child up to
+// the next 16-byte boundary are set to 0xff (never read as nodes).
+__global__ void __launch_bounds__(256) k_splice(const PlanDev* plans, uint32_t count,
+                                                const DirEntry* dir, const Extent* ext,
+                                                const uint64_t* child_off, const uint64_t* child_size,
+                                                uint8_t* arena) {
+    for (uint32_t c = blockIdx.x; c < count; c += gridDim.x) {
+        const PlanDev p = plans[c];
+        const Extent x = ext[c];
+        const uint8_t* mum = dir[p.mum].ptr;
+        const uint8_t* dad = dir[p.dad].ptr;
+        const uint64_t mn = dir[p.mum].size;
+        const uint64_t b1 = x.ms;                      // end of segment A
+        const uint64_t b2 = b1 + (x.de - x.ds);        // end of segment B
+        const uint64_t cn = child_size[c];
+        uint32_t* dst = reinterpret_cast<uint32_t*>(arena + child_off[c]);
+        const uint64_t nwords = ((cn + 15) & ~uint64_t(15)) / 4;
+        (void)mn;
+        for (uint64_t w = threadIdx.x; w < nwords; w += blockDim.x) {
+            const uint64_t q = 4 * w;
+            const bool edge = (q < b1 && b1 < q + 4) || (q < b2 && b2 < q + 4) || (q + 4 > cn);
+            uint32_t v;
+            if (!edge) {
+                const uint8_t* src = q < b1 ? mum + q : q < b2 ? dad + x.ds + (q - b1)
+                                                                : mum + x.me + (q - b2);
+                v = ld_word_unaligned(src);
+            } else {
+                v = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint64_t pos = q + k;
+                    uint32_t b = 0xffu;
+                    if (pos < cn) b = pos < b1 ? mum[pos] : pos < b2 ? dad[x.ds + (pos - b1)]
+                                                                    : mum[x.me + (pos - b2)];
+                    v |= b << (8 * k);
+                }
+            }
+            dst[w] = v;
+        }
+    }
+}
+
+}  // namespace ltgp_dev

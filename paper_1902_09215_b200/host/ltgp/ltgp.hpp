@@ -1,0 +1,173 @@
+// ltgp.hpp — the reference's host-side population API (namespace ltgp, same
+// names, argument meaning and error behaviour), re-implemented so that the
+// evaluation and crossover hot path runs on the B200 engine behind
+// include/ltgp_cuda.h. Each declaration cites the reference header it mirrors
+// (/root/reference/proj/include/ltgp/).
+//
+// What differs from the reference, by design:
+//  * Individual::genome may be empty after execute_generation: children live
+//    in the engine's device arena; fitness/hits/size/depth are filled from
+//    the engine's records, and plan_generation draws points from
+//    Individual::size.
+//  * ExecContext carries the engine handle (an extra trailing member; the
+//    reference's four members keep their meaning).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <limits>
+#include <random>
+#include <span>
+#include <stdexcept>
+#include <vector>
+
+#include "../../../include/ltgp_cuda.h"
+
+namespace ltgp {
+
+inline constexpr std::size_t kLaneWidth = 48;           // common.hpp:10-11
+inline constexpr std::uint8_t kOpAdd = 0, kOpSub = 1, kOpMul = 2, kOpDiv = 3, kOpX = 4;
+inline constexpr std::uint8_t kOpFirstConstant = 5;     // opcodes.hpp:10-15
+inline constexpr int kFunctionCount = 4, kConstantCount = 250;
+constexpr bool is_function(std::uint8_t op) { return op < kFunctionCount; }  // opcodes.hpp:22
+
+// rng.hpp:9-14
+inline constexpr std::uint64_t splitmix64(std::uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+// rng.hpp:20-51: sequential stream; value mappings by hand so every output
+// is a pure function of the seed.
+class Rng {
+public:
+    explicit Rng(std::uint64_t seed) : engine_(splitmix64(seed)) {}
+    std::uint64_t below(std::uint64_t n) {
+        ++draws_;
+        unsigned __int128 m = static_cast<unsigned __int128>(engine_()) * n;
+        auto lo = static_cast<std::uint64_t>(m);
+        if (lo < n) {
+            const std::uint64_t threshold = (0 - n) % n;
+            while (lo < threshold) {
+                m = static_cast<unsigned __int128>(engine_()) * n;
+                lo = static_cast<std::uint64_t>(m);
+            }
+        }
+        return static_cast<std::uint64_t>(m >> 64);
+    }
+    float uniform_pm1() {
+        ++draws_;
+        const double u = static_cast<double>(engine_() >> 11) * 0x1.0p-53;
+        return static_cast<float>(2.0 * u - 1.0);
+    }
+    std::uint64_t draw_count() const { return draws_; }
+
+private:
+    std::mt19937_64 engine_;
+    std::uint64_t draws_ = 0;
+};
+
+// genome.hpp:19-38
+class Genome {
+public:
+    Genome() = default;
+    explicit Genome(std::vector<std::uint8_t> ops) : ops_(std::move(ops)) {}
+    std::size_t size() const noexcept { return ops_.size(); }
+    bool empty() const noexcept { return ops_.empty(); }
+    std::uint8_t operator[](std::size_t i) const noexcept { return ops_[i]; }
+    const std::uint8_t* data() const noexcept { return ops_.data(); }
+    std::span<const std::uint8_t> ops() const noexcept { return {ops_.data(), ops_.size()}; }
+    void release() noexcept { std::vector<std::uint8_t>().swap(ops_); }
+    friend bool operator==(const Genome&, const Genome&) = default;
+
+private:
+    std::vector<std::uint8_t> ops_;
+};
+
+// sextic.hpp:25-31
+struct TestSuite {
+    alignas(64) float inputs[kLaneWidth]{};
+    alignas(64) float targets[kLaneWidth]{};
+    float constants[kConstantCount]{};
+};
+
+float target(float x);                       // sextic.hpp:33-35
+TestSuite make_suite(Rng& rng);              // sextic.hpp:50
+TestSuite make_suite(std::uint64_t seed);    // sextic.hpp:51
+std::uint64_t suite_seed(std::uint64_t run_seed);  // driver.hpp:17-19
+
+Genome gen_full(Rng& rng, int target_depth, std::size_t capacity);   // genome.hpp:61
+Genome gen_grow(Rng& rng, int max_depth, std::size_t capacity);      // genome.hpp:64
+std::vector<Genome> ramped_half_and_half(Rng& rng, std::size_t count, std::size_t capacity,
+                                         int min_depth = 2, int max_depth = 6);  // genome.hpp:68
+Genome random_tree_of_size(Rng& rng, std::size_t nodes);             // bench.hpp:15
+void random_tree_of_size(Rng& rng, std::size_t nodes, std::uint8_t* out);
+
+// evolve.hpp:17-23
+struct Individual {
+    Genome genome;
+    float fitness = std::numeric_limits<float>::quiet_NaN();
+    std::int32_t hits = 0;
+    std::uint32_t size = 0;
+    std::uint32_t depth = 0;
+};
+
+using CrossoverPlan = ltgp_plan;  // evolve.hpp:27-32 (same field order)
+
+enum class TerminationReason { kMaxGenerations, kSizeLimitHit, kMemoryBudgetExceeded };  // evolve.hpp:34
+
+struct RunConfig {  // evolve.hpp:37-47
+    std::uint32_t population_size = 4000;
+    std::uint32_t max_generations = 10000;
+    std::uint64_t node_limit = 15'000'000;
+    std::uint32_t tournament_size = 7;
+    std::uint32_t worker_count = 1;
+    std::uint64_t seed = 1;
+    std::uint64_t memory_budget_bytes = 0;
+    bool streaming_memory = false;
+    double stack_safety = 2.0;
+};
+void validate(const RunConfig& config);  // evolve.hpp:49-50, throws std::invalid_argument
+
+struct WorkerState {};   // evolve.hpp:73-77: per-worker stacks live on the GPU
+struct MemoryGauge {     // evolve.hpp:52-71 (live genome accounting)
+    void add(std::int64_t n = 1) { live_ += n; if (live_ > high_) high_ = live_; }
+    void sub(std::int64_t n = 1) { live_ -= n; }
+    std::int64_t live() const { return live_; }
+    std::int64_t high_water() const { return high_; }
+private:
+    std::int64_t live_ = 0, high_ = 0;
+};
+
+struct ExecContext {     // evolve.hpp:95-100, plus the engine handle
+    const TestSuite& suite;
+    const RunConfig& config;
+    std::vector<WorkerState>& pool;
+    MemoryGauge& gauge;
+    ltgp_engine* engine = nullptr;
+};
+
+struct ExecOutcome { bool size_limit_hit = false; };  // evolve.hpp:102-104
+
+inline bool fitness_better(float a, float b) {  // eval.hpp:90-94
+    if (a != a) return false;
+    if (b != b) return true;
+    return a < b;
+}
+inline bool fitness_tied(float a, float b) { return (a != a && b != b) || a == b; }  // eval.hpp:96-98
+
+std::size_t tournament(Rng& rng, std::span<const Individual> population, std::uint32_t k);  // evolve.hpp:82
+std::vector<CrossoverPlan> plan_generation(Rng& rng, std::span<const Individual> population,
+                                           std::uint32_t tournament_size);  // evolve.hpp:86-87
+
+// evolve.hpp:106-117 — the drop-in boundary, on the engine.
+void evaluate_population(std::vector<Individual>& population, ExecContext ctx);
+ExecOutcome execute_generation(std::span<const CrossoverPlan> plans, std::vector<Individual>& parents,
+                               std::vector<Individual>& children, ExecContext ctx);
+
+// Throws std::runtime_error with ltgp_last_error() on an engine failure.
+void check(int status);
+
+}  // namespace ltgp

@@ -1,0 +1,432 @@
+// ltgp_host.cpp — libltgp_host.so: the reference's host-side population API
+// (ltgp/ltgp.hpp) on top of the B200 engine (include/ltgp_cuda.h).
+//
+// Everything here is the *caller* side of the hot path that the reference
+// keeps sequential on the host: the RNG stream, tree
+// construction, tournament selection and crossover planning. Evaluation and
+// splicing go through the C ABI to the GPU.
+
+#include "ltgp/ltgp.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <thread>
+
+#include "../../include/ltgp_host.h"
+
+namespace ltgp {
+
+void check(int status) {
+    if (status != 0) throw std::runtime_error(std::string("ltgp engine: ") + ltgp_last_error());
+}
+
+// sextic.hpp:33-35: y = x*x*(x-1)*(x-1)*(x+1)*(x+1), left to right, float.
+float target(float x) {
+    float y = x * x;
+    y *= (x - 1.0f);
+    y *= (x - 1.0f);
+    y *= (x + 1.0f);
+    y *= (x + 1.0f);
+    return y;
+}
+
+namespace {
+// sextic.hpp:37-40: 9 significant digits (lossless for float).
+float canonical(float v) {
+    char buf[48];
+    std::snprintf(buf, sizeof buf, "%.9g", static_cast<double>(v));
+    return std::strtof(buf, nullptr);
+}
+}  // namespace
+
+// sextic.hpp:42-51: 48 cases first (x, y after the text round trip), then
+// 250 distinct millesimal-grid constants by partial Fisher-Yates
+// (below(2001 - j)), each parsed from its 3-decimal text, sorted.
+TestSuite make_suite(Rng& rng) {
+    TestSuite s;
+    for (std::size_t l = 0; l < kLaneWidth; ++l) {
+        const float x = canonical(rng.uniform_pm1());
+        s.inputs[l] = x;
+        s.targets[l] = canonical(target(x));
+    }
+    int grid[2001];
+    for (int k = 0; k < 2001; ++k) grid[k] = k;
+    for (int j = 0; j < kConstantCount; ++j) {
+        const auto k = static_cast<std::size_t>(j) + rng.below(static_cast<std::uint64_t>(2001 - j));
+        std::swap(grid[j], grid[k]);
+    }
+    for (int j = 0; j < kConstantCount; ++j) {
+        const int m = grid[j] - 1000;
+        char buf[32];
+        std::snprintf(buf, sizeof buf, "%s%d.%03d", m < 0 ? "-" : "", std::abs(m) / 1000, std::abs(m) % 1000);
+        s.constants[j] = std::strtof(buf, nullptr);
+    }
+    std::sort(s.constants, s.constants + kConstantCount);
+    return s;
+}
+
+TestSuite make_suite(std::uint64_t seed) {
+    Rng rng(seed);
+    return make_suite(rng);
+}
+
+std::uint64_t suite_seed(std::uint64_t run_seed) { return splitmix64(run_seed ^ 0x53554954ull); }
+
+namespace {
+// Prefix-order construction shared by gen_full / gen_grow (genome.hpp:59-64,
+// SPEC.md:72-89): function draws below(4), terminal draws 4+below(251), a
+// grow node above the cap draws below(255) (one draw per opcode).
+Genome build(Rng& rng, int cap_depth, bool full, std::size_t capacity) {
+    std::vector<std::uint8_t> ops;
+    std::vector<int> todo{1};
+    while (!todo.empty()) {
+        const int d = todo.back();
+        todo.pop_back();
+        std::uint8_t op;
+        if (d >= cap_depth) op = static_cast<std::uint8_t>(4 + rng.below(251));
+        else if (full) op = static_cast<std::uint8_t>(rng.below(4));
+        else op = static_cast<std::uint8_t>(rng.below(255));
+        ops.push_back(op);
+        if (ops.size() > capacity) throw std::length_error("tree exceeds capacity");
+        if (is_function(op)) {
+            todo.push_back(d + 1);
+            todo.push_back(d + 1);
+        }
+    }
+    return Genome(std::move(ops));
+}
+}  // namespace
+
+Genome gen_full(Rng& rng, int target_depth, std::size_t capacity) {
+    if (target_depth < 1) throw std::invalid_argument("depth < 1");
+    if (target_depth >= 64 || ((std::size_t{1} << target_depth) - 1) > capacity)
+        throw std::length_error("full tree exceeds capacity");
+    return build(rng, target_depth, true, capacity);
+}
+
+Genome gen_grow(Rng& rng, int max_depth, std::size_t capacity) {
+    if (max_depth < 1) throw std::invalid_argument("depth < 1");
+    return build(rng, max_depth, false, capacity);
+}
+
+// genome.hpp:66-69: depth dmin + (i/2) % span, even i
+// full, odd i grow.
+std::vector<Genome> ramped_half_and_half(Rng& rng, std::size_t count, std::size_t capacity,
+                                         int min_depth, int max_depth) {
+    std::vector<Genome> out;
+    out.reserve(count);
+    const std::size_t span = static_cast<std::size_t>(max_depth - min_depth + 1);
+    for (std::size_t i = 0; i < count; ++i) {
+        const int d = min_depth + static_cast<int>((i / 2) % span);
+        out.push_back((i % 2 == 0) ? gen_full(rng, d, capacity) : gen_grow(rng, d, capacity));
+    }
+    return out;
+}
+
+// bench.hpp:13-15: at a function node draw the opcode
+// below(4), then the left size uniform over odd values in [1, n-2]; a leaf
+// is X or a constant 5+below(250) with equal probability (below(2)).
+void random_tree_of_size(Rng& rng, std::size_t n, std::uint8_t* out) {
+    if (n == 0 || n % 2 == 0) throw std::invalid_argument("tree size must be odd");
+    std::vector<std::uint64_t> todo{n};
+    std::size_t pos = 0;
+    while (!todo.empty()) {
+        const std::uint64_t m = todo.back();
+        todo.pop_back();
+        if (m == 1) {
+            out[pos++] = rng.below(2) == 0 ? kOpX : static_cast<std::uint8_t>(kOpFirstConstant + rng.below(250));
+            continue;
+        }
+        out[pos++] = static_cast<std::uint8_t>(rng.below(4));
+        const std::uint64_t left = 2 * rng.below((m - 1) / 2) + 1;
+        todo.push_back(m - 1 - left);
+        todo.push_back(left);
+    }
+}
+
+Genome random_tree_of_size(Rng& rng, std::size_t n) {
+    std::vector<std::uint8_t> ops(n);
+    random_tree_of_size(rng, n, ops.data());
+    return Genome(std::move(ops));
+}
+
+void validate(const RunConfig& c) {
+    if (c.population_size < 2) throw std::invalid_argument("population_size < 2");
+    if (c.node_limit < 63) throw std::invalid_argument("node_limit < 63");
+    if (c.tournament_size < 1) throw std::invalid_argument("tournament_size < 1");
+}
+
+// evolve.hpp:79-82
+std::size_t tournament(Rng& rng, std::span<const Individual> pop, std::uint32_t k) {
+    const std::uint64_t M = pop.size();
+    std::size_t best = static_cast<std::size_t>(rng.below(M));
+    std::uint64_t ties = 1;
+    for (std::uint32_t i = 1; i < k; ++i) {
+        const std::size_t idx = static_cast<std::size_t>(rng.below(M));
+        if (fitness_better(pop[idx].fitness, pop[best].fitness)) {
+            best = idx;
+            ties = 1;
+        } else if (fitness_tied(pop[idx].fitness, pop[best].fitness)) {
+            if (rng.below(ties + 1) == 0) best = idx;
+            ++ties;
+        }
+    }
+    return best;
+}
+
+// evolve.hpp:84-87
+std::vector<CrossoverPlan> plan_generation(Rng& rng, std::span<const Individual> pop, std::uint32_t k) {
+    std::vector<CrossoverPlan> plans(pop.size());
+    for (auto& p : plans) {
+        p.mum_index = static_cast<std::uint32_t>(tournament(rng, pop, k));
+        p.dad_index = static_cast<std::uint32_t>(tournament(rng, pop, k));
+        p.mum_pt = static_cast<std::uint32_t>(rng.below(pop[p.mum_index].size));
+        p.dad_pt = static_cast<std::uint32_t>(rng.below(pop[p.dad_index].size));
+    }
+    return plans;
+}
+
+namespace {
+void fill(Individual& ind, const ltgp_record& r) {
+    ind.fitness = r.fitness;
+    ind.hits = r.hits;
+    ind.size = r.size;
+    ind.depth = r.depth;
+}
+}  // namespace
+
+// evolve.hpp:108-109 on the engine: upload host genomes, evaluate every slot.
+void evaluate_population(std::vector<Individual>& population, ExecContext ctx) {
+    if (!ctx.engine) throw std::invalid_argument("ExecContext.engine is null");
+    check(ltgp_set_suite(ctx.engine, ctx.suite.inputs, ctx.suite.targets, ctx.suite.constants));
+    std::vector<const std::uint8_t*> ptrs(population.size());
+    std::vector<std::uint64_t> sizes(population.size());
+    for (std::size_t i = 0; i < population.size(); ++i) {
+        ptrs[i] = population[i].genome.data();
+        sizes[i] = population[i].genome.size();
+    }
+    check(ltgp_upload_population(ctx.engine, static_cast<std::uint32_t>(population.size()), ptrs.data(),
+                                 sizes.data()));
+    std::vector<ltgp_record> rec(population.size());
+    check(ltgp_evaluate_population(ctx.engine, rec.data(), nullptr));
+    for (std::size_t i = 0; i < population.size(); ++i) fill(population[i], rec[i]);
+}
+
+// evolve.hpp:111-117 on the engine. `parents` must be the engine's current
+// population (from evaluate_population or a previous execute_generation).
+ExecOutcome execute_generation(std::span<const CrossoverPlan> plans, std::vector<Individual>& parents,
+                               std::vector<Individual>& children, ExecContext ctx) {
+    if (!ctx.engine) throw std::invalid_argument("ExecContext.engine is null");
+    if (plans.size() != parents.size()) throw std::invalid_argument("one plan per child slot");
+    std::vector<ltgp_record> rec(plans.size());
+    int hit = 0;
+    check(ltgp_execute_generation(ctx.engine, plans.data(), static_cast<std::uint32_t>(plans.size()),
+                                  rec.data(), &hit));
+    if (hit) return ExecOutcome{true};
+    children.resize(plans.size());
+    for (std::size_t i = 0; i < plans.size(); ++i) {
+        children[i].genome.release();  // device resident (ltgp_download_genome)
+        fill(children[i], rec[i]);
+    }
+    ctx.gauge.add(static_cast<std::int64_t>(plans.size()));
+    ctx.gauge.sub(static_cast<std::int64_t>(parents.size()));
+    return ExecOutcome{false};
+}
+
+}  // namespace ltgp
+
+using namespace ltgp;
+
+extern "C" {
+
+uint64_t ltgp_host_splitmix64(uint64_t x) { return splitmix64(x); }
+uint64_t ltgp_host_suite_seed(uint64_t s) { return suite_seed(s); }
+
+void ltgp_host_make_suite(uint64_t seed, float* in, float* tg, float* cs) {
+    const TestSuite s = make_suite(seed);
+    std::memcpy(in, s.inputs, sizeof s.inputs);
+    std::memcpy(tg, s.targets, sizeof s.targets);
+    std::memcpy(cs, s.constants, sizeof s.constants);
+}
+
+uint64_t ltgp_host_tree_seed(uint64_t seed, uint32_t i) {
+    return splitmix64(seed ^ (0x7265657274ull + (uint64_t)i * 0x9e3779b97f4a7c15ull));
+}
+
+int ltgp_host_random_tree_of_size(uint64_t seed, uint64_t n, uint8_t* out) {
+    try {
+        Rng rng(seed);
+        random_tree_of_size(rng, n, out);
+        return 0;
+    } catch (...) {
+        return -1;
+    }
+}
+
+uint64_t ltgp_host_corpus(uint64_t seed, uint32_t M, double lg_lo, double lg_hi, uint32_t first,
+                          uint32_t count, uint8_t* buf, uint64_t* offsets, uint64_t* sizes, int threads) {
+    Rng rng(seed);
+    for (uint32_t i = 0; i < M; ++i) {
+        const double u = static_cast<double>(rng.below(1ull << 53)) * 0x1.0p-53;
+        uint64_t n = static_cast<uint64_t>(std::floor(std::pow(10.0, lg_lo + (lg_hi - lg_lo) * u)));
+        sizes[i] = n | 1u;  // odd
+    }
+    if (first > M) first = M;
+    if (count > M - first) count = M - first;
+    uint64_t total = 0;
+    for (uint32_t j = 0; j < count; ++j) {
+        if (offsets) offsets[j] = total;
+        total += (sizes[first + j] + 15) & ~uint64_t(15);
+    }
+    if (!buf || !offsets) return total;
+    if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+    std::atomic<uint32_t> next{0};
+    auto work = [&]() {
+        for (uint32_t j; (j = next.fetch_add(1)) < count;) {
+            const uint32_t i = first + j;
+            Rng r(ltgp_host_tree_seed(seed, i));
+            random_tree_of_size(r, sizes[i], buf + offsets[j]);
+            const uint64_t pad = ((sizes[i] + 15) & ~uint64_t(15)) - sizes[i];
+            std::memset(buf + offsets[j] + sizes[i], 0xff, pad);
+        }
+    };
+    std::vector<std::thread> ts;
+    for (int t = 0; t < threads; ++t) ts.emplace_back(work);
+    for (auto& t : ts) t.join();
+    return total;
+}
+
+// Remy's algorithm: start from one leaf; n_internal times pick a uniform
+// node x and replace it by a new function node whose children are x and a
+// new leaf (the new leaf left or right with equal probability). Then label
+// in prefix order as in config 3.
+int ltgp_host_remy_tree(uint64_t seed, uint64_t n, uint8_t* out) {
+    if (n == 0 || n % 2 == 0 || n > 0xfffffffeull) return -1;
+    Rng rng(seed);
+    const uint32_t total = static_cast<uint32_t>(n);
+    std::vector<uint32_t> left(total, UINT32_MAX), right(total, UINT32_MAX), parent(total, UINT32_MAX);
+    uint32_t root = 0;
+    for (uint32_t k = 0; 2 * k + 1 < total; ++k) {
+        const uint32_t x = static_cast<uint32_t>(rng.below(2ull * k + 1));
+        const uint32_t a = 2 * k + 1, b = 2 * k + 2;
+        const uint32_t p = parent[x];
+        if (p == UINT32_MAX) root = a;
+        else if (left[p] == x) left[p] = a;
+        else right[p] = a;
+        parent[a] = p;
+        if (rng.below(2) == 0) { left[a] = x; right[a] = b; }
+        else { left[a] = b; right[a] = x; }
+        parent[x] = a;
+        parent[b] = a;
+    }
+    std::vector<uint32_t> todo{root};
+    uint64_t pos = 0;
+    while (!todo.empty()) {
+        const uint32_t v = todo.back();
+        todo.pop_back();
+        if (left[v] == UINT32_MAX) {
+            out[pos++] = rng.below(2) == 0 ? kOpX : static_cast<uint8_t>(kOpFirstConstant + rng.below(250));
+        } else {
+            out[pos++] = static_cast<uint8_t>(rng.below(4));
+            todo.push_back(right[v]);
+            todo.push_back(left[v]);
+        }
+    }
+    return pos == n ? 0 : -1;
+}
+
+uint64_t ltgp_host_ramped(uint64_t seed, uint32_t count, uint64_t capacity, int dmin, int dmax, uint8_t* out,
+                          uint64_t out_cap, uint64_t* sizes) {
+    try {
+        Rng rng(seed);
+        const auto pop = ramped_half_and_half(rng, count, capacity, dmin, dmax);
+        uint64_t pos = 0;
+        for (uint32_t i = 0; i < count; ++i) {
+            if (pos + pop[i].size() > out_cap) return 0;
+            std::memcpy(out + pos, pop[i].data(), pop[i].size());
+            sizes[i] = pop[i].size();
+            pos += pop[i].size();
+        }
+        return pos;
+    } catch (...) {
+        return 0;
+    }
+}
+
+void ltgp_host_plan_generation(uint64_t seed, uint32_t M, const ltgp_record* rec, uint32_t k, ltgp_plan* out) {
+    std::vector<Individual> pop(M);
+    for (uint32_t i = 0; i < M; ++i) {
+        pop[i].fitness = rec[i].fitness;
+        pop[i].size = rec[i].size;
+    }
+    Rng rng(seed);
+    const auto plans = plan_generation(rng, pop, k);
+    std::copy(plans.begin(), plans.end(), out);
+}
+
+// run.hpp:33-36 on the engine.
+int64_t ltgp_host_run(ltgp_engine* e, uint32_t M, uint32_t G, uint64_t node_limit, uint32_t k, uint64_t seed,
+                      const char* dump_path, int* reason, uint64_t* nodes, double* eval_seconds) {
+    try {
+        RunConfig cfg;
+        cfg.population_size = M;
+        cfg.max_generations = G;
+        cfg.node_limit = node_limit;
+        cfg.tournament_size = k;
+        cfg.seed = seed;
+        validate(cfg);
+        const TestSuite suite = make_suite(suite_seed(seed));
+        Rng rng(seed);
+        std::vector<Individual> pop(M), next;
+        auto genomes = ramped_half_and_half(rng, M, node_limit, 2, 6);
+        for (uint32_t i = 0; i < M; ++i) pop[i].genome = std::move(genomes[i]);
+        std::vector<WorkerState> pool(1);
+        MemoryGauge gauge;
+        gauge.add(M);
+        ExecContext ctx{suite, cfg, pool, gauge, e};
+        FILE* dump = dump_path ? std::fopen(dump_path, "w") : nullptr;
+        auto write_dump = [&](uint32_t gen) {  // stats.hpp:104-107
+            if (!dump) return;
+            for (uint32_t i = 0; i < M; ++i) {
+                uint32_t bits;
+                std::memcpy(&bits, &pop[i].fitness, 4);
+                if (pop[i].fitness != pop[i].fitness) bits = 0x7fc00000u;
+                std::fprintf(dump, "%u %u %u %u %d %08x\n", gen, i, pop[i].size, pop[i].depth, pop[i].hits, bits);
+            }
+        };
+        *reason = 0;
+        *nodes = 0;
+        double secs = 0.0;
+        ltgp_stats st;
+        evaluate_population(pop, ctx);
+        check(ltgp_get_stats(e, &st));
+        secs += st.eval_seconds;
+        for (auto& ind : pop) *nodes += ind.size;
+        write_dump(0);
+        int64_t done = 0;
+        for (uint32_t gen = 1; gen <= G; ++gen) {
+            const auto plans = plan_generation(rng, pop, k);
+            const ExecOutcome o = execute_generation(plans, pop, next, ctx);
+            if (o.size_limit_hit) { *reason = 1; break; }
+            std::swap(pop, next);
+            check(ltgp_get_stats(e, &st));
+            secs += st.eval_seconds;
+            for (auto& ind : pop) *nodes += ind.size;
+            done = gen;
+            write_dump(gen);
+        }
+        if (dump) std::fclose(dump);
+        if (eval_seconds) *eval_seconds = secs;
+        return done;
+    } catch (const std::exception& ex) {
+        std::fprintf(stderr, "ltgp_host_run: %s\n", ex.what());
+        return -1;
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,55 @@
+"""The drop-in boundary without a GPU (CPU only): every symbol the headers
+in include/ declare is exported by the in-tree libraries, and the product
+fails loudly (no silent CPU fallback) when no B200 is visible."""
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_1902_09215_b200 as ltgp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared(header):
+    text = open(os.path.join(ROOT, "include", header)).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(ltgp_[a-z0-9_]+)\s*\(", text)))
+
+
+def exported(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", lib], capture_output=True, text=True, check=True).stdout
+    return {line.split()[-1] for line in out.splitlines() if " T " in line}
+
+
+@pytest.mark.parametrize("header,lib", [("ltgp_cuda.h", ltgp.CUDA_LIB_PATH), ("ltgp_host.h", ltgp.HOST_LIB_PATH)])
+def test_every_declared_symbol_is_exported(header, lib):
+    names = declared(header)
+    assert len(names) > 5
+    missing = [n for n in names if n not in exported(lib)]
+    assert not missing, missing
+
+
+def test_ctypes_binding_covers_header():
+    assert sorted(ltgp._CUDA_SIGS) == declared("ltgp_cuda.h")
+    assert sorted(ltgp._HOST_SIGS) == declared("ltgp_host.h")
+
+
+def test_libraries_load_and_bind():
+    lib = ltgp.cuda_lib()
+    assert b"sm_100a" in lib.ltgp_version()
+    ltgp.host_lib()
+
+
+def test_cubin_is_sm100a():
+    out = subprocess.run(["cuobjdump", "-lelf", ltgp.CUDA_LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(ltgp.EngineError):
+        ltgp.Engine([0])

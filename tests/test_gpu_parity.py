@@ -1,0 +1,227 @@
+"""Parity of the B200 engine with the CPU oracle (run on the GPU box: -m gpu).
+
+Every test goes through the C ABI (include/ltgp_cuda.h) via the package's
+ctypes binding. Tolerance: bit-exact per case (modulo NaN payload, which
+differs between x86 and the GPU — SURVEY.md App. A #14) and bit-exact
+fitness / hits / size / depth.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1902_09215_b200 as ltgp
+from tests._oracle import REC, same_bits
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+ADD, SUB, MUL, DIV, X = 0, 1, 2, 3, 4
+
+
+@pytest.fixture(scope="module")
+def suite():
+    return ltgp.make_suite(ltgp.suite_seed(1))
+
+
+def engine(suite, devices=(0,), chunk=0):
+    e = ltgp.Engine(list(devices), node_limit=2**40, chunk_nodes=chunk)
+    e.set_suite(*suite)
+    return e
+
+
+def pack(genomes):
+    sizes = np.array([g.size for g in genomes], np.uint64)
+    offs = np.zeros(len(genomes), np.uint64)
+    o = 0
+    for k, s in enumerate(sizes):
+        offs[k] = o
+        o += (int(s) + 15) // 16 * 16
+    buf = np.full(o + 64, 0xFF, np.uint8)
+    for k, g in enumerate(genomes):
+        buf[int(offs[k]):int(offs[k]) + g.size] = g
+    return buf, offs, sizes
+
+
+def assert_records_equal(got, exp):
+    assert same_bits(got["fitness"], exp["fitness"])
+    assert np.array_equal(got["hits"], exp["hits"])
+    assert np.array_equal(got["size"], exp["size"])
+    assert np.array_equal(got["depth"], exp["depth"])
+
+
+def check_population(oracle, suite, genomes, chunk=0, devices=(0,)):
+    with engine(suite, devices, chunk) as e:
+        e.upload_population(genomes)
+        rec, outs = e.evaluate_outputs()
+    buf, offs, sizes = pack(genomes)
+    exp = oracle.evaluate_population(buf, offs, sizes, suite, threads=0)
+    for k, g in enumerate(genomes):
+        o, _ = oracle.eval_batch(g, suite[0], suite[2])
+        assert same_bits(outs[k], o), f"tree {k} (size {g.size}) per-case outputs differ"
+    assert_records_equal(rec, exp)
+    return rec
+
+
+def test_spec_genomes(oracle, suite):
+    i, t, c = suite
+    with engine(suite) as e:
+        assert same_bits(e.eval_batch(np.array([X], np.uint8)), i)
+        assert same_bits(e.eval_batch(np.array([5 + 9], np.uint8)), np.full(48, c[9]))
+        for g in ([ADD, X, X], [SUB, MUL, X, X, X], [DIV, X, SUB, X, X], [DIV, X, 5 + 0]):
+            g = np.array(g, np.uint8)
+            o, _ = oracle.eval_batch(g, i, c)
+            assert same_bits(e.eval_batch(g), o), g
+
+
+def test_golden_fixture_trees(suite):
+    """Per-case outputs frozen from the oracle (tests/golden/oracle_golden.json)."""
+    g = json.load(open(os.path.join(HERE, "golden", "oracle_golden.json")))
+    with engine(suite) as e:
+        for tr in g["trees"]:
+            tree = ltgp.random_tree_of_size(tr["seed"], tr["n"])
+            out = e.eval_batch(tree)
+            assert out.view(np.uint32).tolist() == tr["outputs_bits"] or \
+                same_bits(out, np.array(tr["outputs_bits"], np.uint32).view(np.float32))
+
+
+def test_config1_population_golden(oracle):
+    """Config 1: pop 48 ramped half-and-half, one evaluation; golden records."""
+    g = json.load(open(os.path.join(HERE, "golden", "oracle_golden.json")))
+    for s, d in g["c1"].items():
+        suite = ltgp.make_suite(ltgp.suite_seed(int(s)))
+        genomes = [np.array(x, np.uint8) for x in d["genomes"]]
+        with engine(suite) as e:
+            e.upload_population(genomes)
+            rec = e.evaluate_population()
+        assert rec["fitness"].view(np.uint32).tolist() == d["fitness_bits"]
+        assert rec["hits"].tolist() == d["hits"]
+        assert rec["size"].tolist() == d["size"]
+        assert rec["depth"].tolist() == d["depth"]
+
+
+@pytest.mark.parametrize("chunk", [64, 1024, 16384])
+def test_config3_small_chunked(oracle, suite, chunk):
+    """Config-3 trees (uniform prefix splits) across chunk sizes: chunk
+    summaries + spine combine must reproduce the sequential scan bit for bit."""
+    buf, offs, sizes = ltgp.corpus(5, 40, 1.0, 4.7)
+    genomes = [buf[int(o):int(o) + int(n)].copy() for o, n in zip(offs, sizes)]
+    check_population(oracle, suite, genomes, chunk=chunk)
+
+
+@pytest.mark.parametrize("chunk", [256, 16384])
+def test_remy_deep_trees(oracle, suite, chunk):
+    """Uniform random shapes (config 4 generator): deep stacks exercise the
+    shared-window spill/fill and long spines."""
+    genomes = [ltgp.remy_tree(40 + k, n) for k, n in enumerate((1, 3, 1001, 20001, 200001))]
+    check_population(oracle, suite, genomes, chunk=chunk)
+
+
+def test_adversarial(oracle, suite):
+    c0 = 5 + int(np.argmin(np.abs(suite[2])))  # constant nearest 0 (may be 0.000)
+    gs = []
+    # left chain: DIV(DIV(...(X, c)...)) -> repeated division, underflow to subnormal / 0
+    gs.append(np.array([DIV] * 3000 + [X] + [5 + 200] * 3000, np.uint8))
+    # right chain of MUL: overflow to inf then inf*0 = NaN
+    gs.append(np.array([MUL, 5 + 249] * 2000 + [X], np.uint8))
+    # zero divisors everywhere: x / (x - x) and c / (c - c)
+    gs.append(np.array([DIV, X, SUB, X, X], np.uint8))
+    gs.append(np.array([ADD] * 50 + sum(([DIV, X, SUB, X, X] for _ in range(51)), []), np.uint8))
+    gs.append(np.array([DIV, 5 + 1, c0], np.uint8))
+    # subnormal arithmetic: (c*c*c*...)/x chains
+    gs.append(np.array([SUB] + [MUL] * 40 + [5 + 3] * 41 + [DIV, 5 + 5, X], np.uint8))
+    for chunk in (64, 0):
+        check_population(oracle, suite, gs, chunk=chunk)
+
+
+def test_subtree_extents(oracle, suite):
+    genomes = [ltgp.remy_tree(7, 4001), ltgp.random_tree_of_size(8, 999), np.array([X], np.uint8)]
+    with engine(suite) as e:
+        e.upload_population(genomes)
+        rng = np.random.default_rng(0)
+        slots, pts = [], []
+        for s, g in enumerate(genomes):
+            for p in list(rng.integers(0, g.size, 200)) + [0, g.size - 1]:
+                slots.append(s)
+                pts.append(int(p))
+        ext = e.subtree_extents(slots, pts)
+    for (s, p), (a, b) in zip(zip(slots, pts), ext):
+        assert (int(a), int(b)) == oracle.subtree_extent(genomes[s], p)
+
+
+def test_execute_generation_children(oracle, suite):
+    """Device splice vs the oracle's crossover, child by child, and records."""
+    genomes = [ltgp.random_tree_of_size(100 + k, 2 * k + 1) for k in range(60)] + \
+              [ltgp.remy_tree(300, 30001)]
+    M = len(genomes)
+    rng = np.random.default_rng(5)
+    plans = np.zeros(M, ltgp.PLAN_DTYPE)
+    plans["mum_index"] = rng.integers(0, M, M)
+    plans["dad_index"] = rng.integers(0, M, M)
+    plans["mum_pt"] = [rng.integers(0, genomes[m].size) for m in plans["mum_index"]]
+    plans["dad_pt"] = [rng.integers(0, genomes[d].size) for d in plans["dad_index"]]
+    for devices in ((0,), (0, 0, 0)):
+        with engine(suite, devices, chunk=512) as e:
+            e.upload_population(genomes)
+            e.evaluate_population()
+            rec, hit = e.execute_generation(plans)
+            assert not hit
+            children = [e.download_genome(c) for c in range(M)]
+        for c in range(M):
+            p = plans[c]
+            exp, h, n = oracle.crossover(genomes[p["mum_index"]], genomes[p["dad_index"]], int(p["mum_pt"]),
+                                         int(p["dad_pt"]), 2**40)
+            assert np.array_equal(children[c], exp), c
+        buf, offs, sizes = pack(children)
+        assert_records_equal(rec, oracle.evaluate_population(buf, offs, sizes, suite))
+
+
+def test_execute_generation_size_limit(suite):
+    genomes = [ltgp.random_tree_of_size(1, 31), ltgp.random_tree_of_size(2, 63)]
+    with ltgp.Engine([0], node_limit=63) as e:
+        e.set_suite(*suite)
+        e.upload_population(genomes)
+        e.evaluate_population()
+        plans = np.zeros(2, ltgp.PLAN_DTYPE)
+        plans[0] = (0, 1, 0, 0)   # child = dad (63 nodes) -> reaches the limit
+        plans[1] = (0, 0, 1, 1)
+        rec, hit = e.execute_generation(plans)
+        assert hit
+        assert np.array_equal(e.download_genome(0), genomes[0])  # population unchanged
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_run_dump_matches_oracle(oracle, tmp_path, seed):
+    """run() on the engine vs the oracle's run(): identical generation dumps
+    (fitness bits, hits, size, depth of every individual, every generation),
+    so selected parents are identical too."""
+    d_ref = tmp_path / "ref.txt"
+    r = oracle.run(48, 40, 10**9, 7, seed, 0, str(d_ref))
+    for devices in ((0,), (0, 0)):
+        d = tmp_path / f"gpu{len(devices)}.txt"
+        with ltgp.Engine(list(devices), node_limit=10**9, chunk_nodes=256) as e:
+            g = e.run(48, 40, 10**9, 7, seed, str(d))
+        assert g["generations"] == r["generations"] == 40
+        assert d.read_bytes() == d_ref.read_bytes()
+
+
+def test_run_size_limit_matches_oracle(oracle, tmp_path):
+    r = oracle.run(48, 300, 200, 7, 4, 0, str(tmp_path / "a"))
+    with ltgp.Engine([0], node_limit=200) as e:
+        g = e.run(48, 300, 200, 7, 4, str(tmp_path / "b"))
+    assert r["reason"] == g["reason"] == 1
+    assert r["generations"] == g["generations"]
+    assert (tmp_path / "a").read_bytes() == (tmp_path / "b").read_bytes()
+
+
+def test_config3_full_size_sampled(oracle, suite):
+    """BASELINE config 3 at full size (4000 trees, 10^4..10^6 nodes): every
+    record compared with the oracle (multi-threaded)."""
+    buf, offs, sizes = ltgp.corpus(1, 4000, 4.0, 6.0)
+    with engine(suite) as e:
+        e.upload_packed(buf, offs, sizes)
+        rec = e.evaluate_population()
+        rec2 = e.evaluate_population()
+    assert rec.tobytes() == rec2.tobytes()  # determinism across launches
+    exp = oracle.evaluate_population(buf, offs, sizes, suite, threads=0)
+    assert_records_equal(rec, exp)

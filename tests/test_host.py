@@ -1,0 +1,65 @@
+"""The C++ host side (libltgp_host.so: Rng, suite, generators, tournament
+and planning — the caller of the hot path) against the oracle (CPU only)."""
+import numpy as np
+
+import paper_1902_09215_b200 as ltgp
+from tests._oracle import REC
+
+
+def test_splitmix_and_suite_seed(oracle):
+    for x in (0, 1, 2, 42, 2**63, 2**64 - 1):
+        assert ltgp.splitmix64(x) == oracle.orc_splitmix64(x)
+        assert ltgp.suite_seed(x) == oracle.orc_suite_seed(x)
+
+
+def test_make_suite_matches_oracle(oracle):
+    for s in (1, 2, 3, 99):
+        a = ltgp.make_suite(ltgp.suite_seed(s))
+        b = oracle.make_suite(oracle.orc_suite_seed(s))
+        for x, y in zip(a, b):
+            assert x.view(np.uint32).tolist() == y.view(np.uint32).tolist()
+        i, t, c = a
+        assert np.all(np.abs(i) <= 1) and len(set(c.tolist())) == 250 and np.all(np.diff(c) > 0)
+
+
+def test_random_tree_of_size_matches_oracle(oracle):
+    for k, n in enumerate((1, 3, 7, 999, 100001)):
+        assert np.array_equal(ltgp.random_tree_of_size(50 + k, n), oracle.random_tree_of_size(50 + k, n))
+
+
+def test_corpus_trees_match_oracle_generator(oracle):
+    buf, offs, sizes = ltgp.corpus(11, 24, 2.0, 4.0)
+    assert np.all(offs % 16 == 0) and np.all(sizes % 2 == 1)
+    assert sizes.min() >= 100 and sizes.max() <= 10001
+    for i in range(24):
+        g = buf[int(offs[i]):int(offs[i]) + int(sizes[i])]
+        assert np.array_equal(g, oracle.random_tree_of_size(ltgp.tree_seed(11, i), int(sizes[i])))
+
+
+def test_remy_tree_valid(oracle):
+    for n in (1, 3, 1001, 200001):
+        g = ltgp.remy_tree(5, n)
+        assert oracle.validate(g)
+    # uniform random shapes are deep: depth ~ 2 sqrt(pi n / 2)
+    g = ltgp.remy_tree(6, 200001)
+    d = oracle.depth(g)
+    assert 0.3 * 2 * np.sqrt(np.pi * 100000) < d < 3 * 2 * np.sqrt(np.pi * 100000)
+
+
+def test_ramped_matches_oracle(oracle):
+    for s in (1, 2, 3):
+        a = ltgp.ramped_half_and_half(s, 48)
+        b = oracle.ramped(s, 48)
+        assert all(np.array_equal(x, y) for x, y in zip(a, b))
+
+
+def test_plan_generation_matches_oracle(oracle):
+    rng = np.random.default_rng(3)
+    rec = np.zeros(500, REC)
+    rec["fitness"] = rng.choice([0.5, 0.25, 0.125, np.nan, 0.3], size=500).astype(np.float32)  # many ties
+    rec["size"] = rng.integers(1, 1000, size=500) | 1
+    for seed in (1, 7):
+        a = ltgp.plan_generation(seed, rec.view(ltgp.RECORD_DTYPE), 7)
+        b = oracle.plan_generation(seed, rec, 7)
+        assert a.tobytes() == b.tobytes()
+        assert np.all(a["mum_pt"] < rec["size"][a["mum_index"]])
