@@ -25,8 +25,8 @@ using namespace ltgp_dev;
 
 namespace {
 
-constexpr int kWarps = 4;            // warps per k_eval CTA
-constexpr uint32_t kWindow = 64;     // shared stack window frames per warp
+constexpr int kWarps = 24;           // warps per k_eval CTA (one CTA per SM)
+constexpr int kWindow = 32;          // shared stack window frames per warp
 constexpr uint32_t kDefaultChunk = 16384;
 constexpr uint32_t kMaxSteps = 1024;
 constexpr uint32_t kMaxFrames = 256;
@@ -110,13 +110,13 @@ inline uint64_t ceil16(uint64_t x) { return (x + 15) & ~uint64_t(15); }
 
 // A set of trees resident on one device: tree i at arena + off[i].
 struct TreeSet {
-    DevBuf arena, off, size;
+    DevBuf arena, off, size, decode;
     std::vector<uint64_t> h_off;
     std::vector<uint32_t> h_size;
     uint32_t count = 0;
     uint64_t bytes = 0;   // used arena bytes
     uint64_t version = 0; // bumped whenever the layout (sizes) changes
-    void release() { arena.release(); off.release(); size.release(); }
+    void release() { arena.release(); off.release(); size.release(); decode.release(); }
 };
 
 uint64_t g_version = 0;
@@ -133,8 +133,13 @@ struct Shard {
     TreeSet scratch;                // ltgp_eval_one
     // evaluation scratch
     DevBuf items, ctrees, hdr, steps, frames, dframes, segs, spill, counters, rec, outs;
+    DevBuf big_steps, big_frames, rerun_items, rerun_slot;  // overflowed chunk summaries
+    bool last_outs = false;
+    uint32_t last_reruns = 0;
     HostBuf h_items, h_ctrees, h_counters;
     uint32_t last_items = 0, last_chunks = 0, last_ctrees = 0;
+    EvalArgs eargs;      // arguments of the last evaluation (for overflow reruns)
+    CombineArgs cargs;
     const TreeSet* items_for = nullptr;  // work list cache: (set, version)
     uint64_t items_version = 0;
     // crossover scratch
@@ -143,7 +148,8 @@ struct Shard {
     void release() {
         set[0].release(); set[1].release(); scratch.release();
         for (DevBuf* b : {&items, &ctrees, &hdr, &steps, &frames, &dframes, &segs, &spill, &counters,
-                          &rec, &outs, &plans, &ext, &csize, &coff, &dir}) b->release();
+                          &rec, &outs, &plans, &ext, &csize, &coff, &dir, &big_steps, &big_frames,
+                          &rerun_items, &rerun_slot}) b->release();
         h_items.release(); h_ctrees.release(); h_counters.release();
         h_csize.release(); h_coff.release(); h_dir.release();
         if (st) { cudaSetDevice(dev); cudaStreamDestroy(st); }
@@ -166,7 +172,8 @@ struct ltgp_engine {
 
 namespace {
 
-size_t eval_smem_bytes() { return kCtabBytes + (size_t)kWarps * (kWindow + 1) * kFrameBytes; }
+size_t eval_smem_bytes() { return EvalLayout<kWarps, kWindow>::kBytes; }
+#define K_EVAL k_eval<kWarps, kWindow>
 
 int init_shard(ltgp_engine* e, Shard& s) {
     CK(cudaSetDevice(s.dev));
@@ -181,9 +188,9 @@ int init_shard(ltgp_engine* e, Shard& s) {
     }
     s.sms = prop.multiProcessorCount;
     const size_t smem = eval_smem_bytes();
-    CK(cudaFuncSetAttribute(k_eval<kWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(K_EVAL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval<kWarps>, kWarps * 32, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K_EVAL, kWarps * 32, smem));
     if (per_sm < 1) { set_err("k_eval does not fit on an SM"); return -1; }
     s.eval_grid = per_sm * s.sms;
     const size_t spill_frames = e->chunk / 2 + 8;
@@ -250,7 +257,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     TRY(s.rec.ensure(sizeof(ltgp_record) * std::max<uint32_t>(ts.count, 1), s.dev));
     if (want_outs) TRY(s.outs.ensure(sizeof(float) * kLanes * std::max<uint32_t>(ts.count, 1), s.dev));
     CK(cudaMemsetAsync(s.counters.p, 0, 64, s.st));
-    EvalArgs a;
+    EvalArgs& a = s.eargs;
     a.arena = ts.arena.as<uint8_t>();
     a.off = ts.off.as<uint64_t>();
     a.size = ts.size.as<uint32_t>();
@@ -266,30 +273,38 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     a.spill_frames = C / 2 + 8;
     a.rec = s.rec.as<float>();
     a.outs = want_outs ? s.outs.as<float>() : nullptr;
-    a.stack_frames = kWindow;
+    a.decode = ts.decode.as<uint4>();
+    a.slot = nullptr;
+    CombineArgs& ca = s.cargs;
+    ca.trees = s.ctrees.as<CombineTree>();
+    ca.n_trees = nct;
+    ca.hdr = s.hdr.as<ChunkHdr>();
+    ca.dframes = s.dframes.as<float2>();
+    ca.segs = s.segs.as<Seg>();
+    ca.rec = s.rec.as<float>();
+    ca.outs = a.outs;
+    ca.counters = s.counters.as<uint32_t>();
+    s.last_outs = want_outs;
+    s.last_reruns = 0;
+    const uint64_t packets = (ts.bytes + 15) / 16;
+    TRY(ts.decode.ensure(std::max<uint64_t>(packets, 1) * 16, s.dev));
+    a.decode = ts.decode.as<uint4>();
     CK(cudaEventRecord(s.ev[0], s.st));
     uint32_t launches = 0;
+    if (packets) {
+        const uint64_t blocks = std::min<uint64_t>((packets + 255) / 256, (uint64_t)s.sms * 16);
+        k_decode<<<(unsigned)blocks, 256, 0, s.st>>>(ts.arena.as<uint4>(), ts.decode.as<uint4>(), packets);
+        CK(cudaGetLastError());
+        ++launches;
+    }
     if (nitems) {
         const int grid = std::min<int>(s.eval_grid, (int)nitems);
-        k_eval<kWarps><<<std::max(grid, 1), kWarps * 32, eval_smem_bytes(), s.st>>>(a, e->suite);
+        K_EVAL<<<std::max(grid, 1), kWarps * 32, eval_smem_bytes(), s.st>>>(a, e->suite);
         CK(cudaGetLastError());
         ++launches;
     }
     CK(cudaEventRecord(s.ev[4], s.st));
     if (nct) {
-        CombineArgs ca;
-        ca.trees = s.ctrees.as<CombineTree>();
-        ca.n_trees = nct;
-        ca.hdr = s.hdr.as<ChunkHdr>();
-        ca.steps = s.steps.as<uint8_t>();
-        ca.frames = s.frames.as<float2>();
-        ca.max_steps = kMaxSteps;
-        ca.max_frames = kMaxFrames;
-        ca.dframes = s.dframes.as<float2>();
-        ca.segs = s.segs.as<Seg>();
-        ca.rec = s.rec.as<float>();
-        ca.outs = a.outs;
-        ca.counters = s.counters.as<uint32_t>();
         const int blocks = (int)std::min<uint32_t>((nct + 3) / 4, (uint32_t)s.sms * 16);
         k_combine<<<blocks, 128, 0, s.st>>>(ca, e->suite);
         CK(cudaGetLastError());
@@ -301,14 +316,70 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     return 0;
 }
 
+// Chunks whose summary (spine steps + frames) outgrew the fixed per-chunk
+// capacity are re-scanned into a dedicated area sized for the worst case
+// of a chunk (every node recorded), then every chunked tree is recombined.
+// Synchronous; only taken when the counters report an overflow.
+int rerun_overflowed(ltgp_engine* e, Shard& s) {
+    CK(cudaSetDevice(s.dev));
+    const uint32_t nch = s.last_chunks;
+    std::vector<ChunkHdr> hdr(nch);
+    CK(cudaMemcpyAsync(hdr.data(), s.hdr.p, sizeof(ChunkHdr) * nch, cudaMemcpyDeviceToHost, s.st));
+    CK(cudaStreamSynchronize(s.st));
+    std::vector<Item> items;
+    std::vector<uint32_t> slots;
+    const Item* all = s.h_items.as<Item>();  // chunk items come first, in chunk order
+    for (uint32_t c = 0; c < nch; ++c)
+        if (hdr[c].flags & 1u) {
+            items.push_back(all[c]);
+            slots.push_back((uint32_t)slots.size());
+        }
+    const uint32_t n = (uint32_t)items.size();
+    if (n == 0) return 0;
+    const uint32_t cap = e->chunk / 2 + 2;  // a chunk holds at most C/2+1 leaves / C/2 ops
+    TRY(s.big_steps.ensure((size_t)n * cap, s.dev));
+    TRY(s.big_frames.ensure((size_t)n * cap * kFrameBytes, s.dev));
+    TRY(s.rerun_items.ensure(sizeof(Item) * n, s.dev));
+    TRY(s.rerun_slot.ensure(sizeof(uint32_t) * n, s.dev));
+    CK(cudaMemcpyAsync(s.rerun_items.p, items.data(), sizeof(Item) * n, cudaMemcpyHostToDevice, s.st));
+    CK(cudaMemcpyAsync(s.rerun_slot.p, slots.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice, s.st));
+    CK(cudaMemsetAsync(s.counters.p, 0, 64, s.st));
+    EvalArgs a = s.eargs;
+    a.items = s.rerun_items.as<Item>();
+    a.n_items = n;
+    a.slot = s.rerun_slot.as<uint32_t>();
+    a.steps = s.big_steps.as<uint8_t>();
+    a.frames = s.big_frames.as<float2>();
+    a.max_steps = cap;
+    a.max_frames = cap;
+    const int grid = std::min<int>(s.eval_grid, (int)n);
+    K_EVAL<<<std::max(grid, 1), kWarps * 32, eval_smem_bytes(), s.st>>>(a, e->suite);
+    CK(cudaGetLastError());
+    const int blocks = (int)std::min<uint32_t>((s.last_ctrees + 3) / 4, (uint32_t)s.sms * 16);
+    k_combine<<<blocks, 128, 0, s.st>>>(s.cargs, e->suite);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(s.h_counters.p, s.counters.p, 64, cudaMemcpyDeviceToHost, s.st));
+    CK(cudaStreamSynchronize(s.st));
+    s.last_reruns = n;
+    e->stats.kernel_launches += 2;
+    return 0;
+}
+
 int check_eval(Shard& s) {
     const uint32_t* c = s.h_counters.as<uint32_t>();
-    if (c[1] & 2u) { set_err("malformed genome (stack underflow or leftover values)"); return -1; }
     if (c[2] != 0 || (c[1] & 1u)) {
-        set_err("chunk summary overflow in %u chunks (raise chunk capacity)", c[2]);
+        set_err("chunk summary overflow in %u chunks", c[2]);
         return -1;
     }
+    if (c[1] & 2u) { set_err("malformed genome (stack underflow or leftover values)"); return -1; }
     return 0;
+}
+
+// After the stream is synchronized: re-run overflowed chunks if any.
+int finish_eval(ltgp_engine* e, Shard& s) {
+    const uint32_t* c = s.h_counters.as<uint32_t>();
+    if (c[2] != 0) TRY(rerun_overflowed(e, s));
+    return check_eval(s);
 }
 
 // Assign contiguous slot ranges to shards, balanced by bytes.
@@ -366,16 +437,17 @@ int upload_tables(Shard& s, TreeSet& ts) {
 
 int collect(ltgp_engine* e, ltgp_record* out, float* outs48) {
     double secs = 0.0, ksecs = 0.0, csecs = 0.0;
-    uint64_t nodes = 0, chunks = 0;
+    uint64_t nodes = 0, chunks = 0, reruns = 0;
     for (Shard& s : e->shards) {
+        if (!s.count) continue;
         CK(cudaSetDevice(s.dev));
-        if (out && s.count) CK(cudaMemcpyAsync(out + s.first, s.rec.p, sizeof(ltgp_record) * s.count,
-                                               cudaMemcpyDeviceToHost, s.st));
-        if (outs48 && s.count) CK(cudaMemcpyAsync(outs48 + (size_t)s.first * kLanes, s.outs.p,
-                                                  sizeof(float) * kLanes * s.count,
-                                                  cudaMemcpyDeviceToHost, s.st));
         CK(cudaStreamSynchronize(s.st));
-        TRY(check_eval(s));
+        TRY(finish_eval(e, s));
+        if (out) CK(cudaMemcpyAsync(out + s.first, s.rec.p, sizeof(ltgp_record) * s.count,
+                                    cudaMemcpyDeviceToHost, s.st));
+        if (outs48) CK(cudaMemcpyAsync(outs48 + (size_t)s.first * kLanes, s.outs.p,
+                                       sizeof(float) * kLanes * s.count, cudaMemcpyDeviceToHost, s.st));
+        CK(cudaStreamSynchronize(s.st));
         float ms = 0.0f;
         CK(cudaEventElapsedTime(&ms, s.ev[0], s.ev[1]));
         secs = std::max(secs, ms * 1e-3);
@@ -386,7 +458,9 @@ int collect(ltgp_engine* e, ltgp_record* out, float* outs48) {
         const TreeSet& ts = s.set[s.cur];
         for (uint32_t i = 0; i < ts.count; ++i) nodes += ts.h_size[i];
         chunks += s.last_chunks;
+        reruns += s.last_reruns;
     }
+    e->stats.last_fallback_items = reruns;
     e->stats.eval_seconds = secs;
     e->stats.eval_kernel_seconds = ksecs;
     e->stats.combine_seconds = csecs;
@@ -572,9 +646,11 @@ int ltgp_eval_one(ltgp_engine* e, const uint8_t* ops, uint64_t n, float* out48) 
     CK(cudaMemcpyAsync(ts.arena.p, h, ceil16(n), cudaMemcpyHostToDevice, s.st));
     TRY(upload_tables(s, ts));
     TRY(launch_eval(e, s, ts, true));
+    CK(cudaStreamSynchronize(s.st));
+    TRY(finish_eval(e, s));
     CK(cudaMemcpyAsync(out48, s.outs.p, sizeof(float) * kLanes, cudaMemcpyDeviceToHost, s.st));
     CK(cudaStreamSynchronize(s.st));
-    return check_eval(s);
+    return 0;
 }
 
 int ltgp_get_stats(ltgp_engine* e, ltgp_stats* out) {
