@@ -287,7 +287,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     s.last_outs = want_outs;
     s.last_reruns = 0;
     const uint64_t packets = (ts.bytes + 15) / 16;
-    TRY(ts.decode.ensure(std::max<uint64_t>(packets, 1) * 16, s.dev));
+    TRY(ts.decode.ensure(std::max<uint64_t>(packets, 1) * 32, s.dev));
     a.decode = ts.decode.as<uint4>();
     CK(cudaEventRecord(s.ev[0], s.st));
     uint32_t launches = 0;

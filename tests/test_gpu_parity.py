@@ -206,9 +206,10 @@ def test_run_dump_matches_oracle(oracle, tmp_path, seed):
 
 
 def test_run_size_limit_matches_oracle(oracle, tmp_path):
-    r = oracle.run(48, 300, 200, 7, 4, 0, str(tmp_path / "a"))
-    with ltgp.Engine([0], node_limit=200) as e:
-        g = e.run(48, 300, 200, 7, 4, str(tmp_path / "b"))
+    # node_limit=63 -> SizeLimitHit within a few generations
+    r = oracle.run(48, 300, 63, 7, 4, 0, str(tmp_path / "a"))
+    with ltgp.Engine([0], node_limit=63) as e:
+        g = e.run(48, 300, 63, 7, 4, str(tmp_path / "b"))
     assert r["reason"] == g["reason"] == 1
     assert r["generations"] == g["generations"]
     assert (tmp_path / "a").read_bytes() == (tmp_path / "b").read_bytes()
