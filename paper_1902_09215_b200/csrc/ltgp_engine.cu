@@ -371,6 +371,7 @@ int check_eval(Shard& s) {
         set_err("chunk summary overflow in %u chunks", c[2]);
         return -1;
     }
+    if (c[1] & 8u) { set_err("k_eval shared-memory layout does not fit"); return -1; }
     if (c[1] & 2u) { set_err("malformed genome (stack underflow or leftover values)"); return -1; }
     return 0;
 }
