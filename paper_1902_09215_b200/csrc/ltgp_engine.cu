@@ -172,6 +172,7 @@ struct ltgp_engine {
 
 namespace {
 
+static_assert(EvalLayout<kWarps, kWindow>::kBytes <= 227u * 1024u, "k_eval needs more than 227 KB of shared memory");
 size_t eval_smem_bytes() { return EvalLayout<kWarps, kWindow>::kBytes; }
 #define K_EVAL k_eval<kWarps, kWindow>
 
