@@ -26,7 +26,7 @@ using namespace ltgp_dev;
 namespace {
 
 constexpr int kWarps = 24;           // warps per k_eval CTA (one CTA per SM)
-constexpr int kWindow = 32;          // shared stack window frames per warp
+constexpr int kWindow = 31;          // shared stack window frames per warp
 constexpr uint32_t kDefaultChunk = 16384;
 constexpr uint32_t kMaxSteps = 1024;
 constexpr uint32_t kMaxFrames = 256;
@@ -274,7 +274,6 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     a.spill_frames = C / 2 + 8;
     a.rec = s.rec.as<float>();
     a.outs = want_outs ? s.outs.as<float>() : nullptr;
-    a.decode = ts.decode.as<uint4>();
     a.slot = nullptr;
     CombineArgs& ca = s.cargs;
     ca.trees = s.ctrees.as<CombineTree>();
@@ -288,13 +287,15 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     s.last_outs = want_outs;
     s.last_reruns = 0;
     const uint64_t packets = (ts.bytes + 15) / 16;
-    TRY(ts.decode.ensure(std::max<uint64_t>(packets, 1) * 32, s.dev));
-    a.decode = ts.decode.as<uint4>();
+    // 64 B lead-in: the fast path prefetches up to two packets before a tree
+    TRY(ts.decode.ensure(std::max<uint64_t>(packets, 1) * 32 + 64, s.dev));
+    uint4* dec = ts.decode.as<uint4>() + 4;
+    a.decode = dec;
     CK(cudaEventRecord(s.ev[0], s.st));
     uint32_t launches = 0;
     if (packets) {
         const uint64_t blocks = std::min<uint64_t>((packets + 255) / 256, (uint64_t)s.sms * 16);
-        k_decode<<<(unsigned)blocks, 256, 0, s.st>>>(ts.arena.as<uint4>(), ts.decode.as<uint4>(), packets);
+        k_decode<<<(unsigned)blocks, 256, 0, s.st>>>(ts.arena.as<uint4>(), dec, packets);
         CK(cudaGetLastError());
         ++launches;
     }
