@@ -287,15 +287,22 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     s.last_outs = want_outs;
     s.last_reruns = 0;
     const uint64_t packets = (ts.bytes + 15) / 16;
-    // 64 B lead-in: the fast path prefetches up to two packets before a tree
-    TRY(ts.decode.ensure(std::max<uint64_t>(packets, 1) * 32 + 64, s.dev));
-    uint4* dec = ts.decode.as<uint4>() + 4;
+    // +1 KB: the fast path stages record groups up to 512 B past an item
+    TRY(ts.decode.ensure(std::max<uint64_t>(packets, 1) * 32 + 1024, s.dev));
+    uint4* dec = ts.decode.as<uint4>();
     a.decode = dec;
+    a.packets = packets;
     CK(cudaEventRecord(s.ev[0], s.st));
     uint32_t launches = 0;
     if (packets) {
         const uint64_t blocks = std::min<uint64_t>((packets + 255) / 256, (uint64_t)s.sms * 16);
         k_decode<<<(unsigned)blocks, 256, 0, s.st>>>(ts.arena.as<uint4>(), dec, packets);
+        CK(cudaGetLastError());
+        ++launches;
+    }
+    if (nitems) {
+        k_plan<<<(nitems + 127) / 128, 128, 0, s.st>>>(s.items.as<Item>(), nitems, ts.off.as<uint64_t>(),
+                                                      reinterpret_cast<uint8_t*>(dec), packets, kWindow);
         CK(cudaGetLastError());
         ++launches;
     }
