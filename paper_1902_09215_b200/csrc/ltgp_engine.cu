@@ -25,11 +25,13 @@ using namespace ltgp_dev;
 
 namespace {
 
-constexpr int kWarps = 24;           // warps per k_eval CTA (one CTA per SM)
-constexpr int kWindow = 31;          // shared stack window frames per warp
+constexpr int kWarps = 28;           // warps per k_eval CTA (one CTA per SM)
+constexpr int kWindow = 25;          // shared stack window frames per warp
 constexpr uint32_t kDefaultChunk = 16384;
 constexpr uint32_t kMaxSteps = 1024;
 constexpr uint32_t kMaxFrames = 256;
+constexpr uint32_t kSpillFrames = 1024;  // per warp; items that need more are re-run
+constexpr int kRerunCtas = 8;
 
 thread_local std::string g_err;
 
@@ -133,7 +135,7 @@ struct Shard {
     TreeSet scratch;                // ltgp_eval_one
     // evaluation scratch
     DevBuf items, ctrees, hdr, steps, frames, dframes, segs, spill, counters, rec, outs;
-    DevBuf big_steps, big_frames, rerun_items, rerun_slot;  // overflowed chunk summaries
+    DevBuf big_steps, big_frames, rerun_items, rerun_slot, ovf, big_spill;  // overflow reruns
     bool last_outs = false;
     uint32_t last_reruns = 0;
     HostBuf h_items, h_ctrees, h_counters;
@@ -149,7 +151,7 @@ struct Shard {
         set[0].release(); set[1].release(); scratch.release();
         for (DevBuf* b : {&items, &ctrees, &hdr, &steps, &frames, &dframes, &segs, &spill, &counters,
                           &rec, &outs, &plans, &ext, &csize, &coff, &dir, &big_steps, &big_frames,
-                          &rerun_items, &rerun_slot}) b->release();
+                          &rerun_items, &rerun_slot, &ovf, &big_spill}) b->release();
         h_items.release(); h_ctrees.release(); h_counters.release();
         h_csize.release(); h_coff.release(); h_dir.release();
         if (st) { cudaSetDevice(dev); cudaStreamDestroy(st); }
@@ -194,8 +196,7 @@ int init_shard(ltgp_engine* e, Shard& s) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K_EVAL, kWarps * 32, smem));
     if (per_sm < 1) { set_err("k_eval does not fit on an SM"); return -1; }
     s.eval_grid = per_sm * s.sms;
-    const size_t spill_frames = e->chunk / 2 + 8;
-    TRY(s.spill.ensure((size_t)s.eval_grid * kWarps * spill_frames * kFrameBytes, s.dev));
+    TRY(s.spill.ensure((size_t)s.eval_grid * kWarps * kSpillFrames * kFrameBytes, s.dev));
     TRY(s.counters.ensure(64, s.dev));
     TRY(s.h_counters.ensure(64));
     return 0;
@@ -271,7 +272,9 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     a.max_steps = kMaxSteps;
     a.max_frames = kMaxFrames;
     a.spill = s.spill.as<float2>();
-    a.spill_frames = C / 2 + 8;
+    a.spill_frames = kSpillFrames;
+    TRY(s.ovf.ensure(sizeof(uint32_t) * std::max<uint32_t>(nitems, 1), s.dev));
+    a.ovf = s.ovf.as<uint32_t>();
     a.rec = s.rec.as<float>();
     a.outs = want_outs ? s.outs.as<float>() : nullptr;
     a.slot = nullptr;
@@ -325,29 +328,31 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     return 0;
 }
 
-// Chunks whose summary (spine steps + frames) outgrew the fixed per-chunk
-// capacity are re-scanned into a dedicated area sized for the worst case
-// of a chunk (every node recorded), then every chunked tree is recombined.
+// Items whose stack outgrew the per-warp spill area, or chunks whose summary
+// outgrew the per-chunk capacity, are re-scanned with worst-case capacities
+// (a chunk of C nodes holds at most C stack values, C spine steps), on a
+// small grid with its own spill area; then every chunked tree is recombined.
 // Synchronous; only taken when the counters report an overflow.
 int rerun_overflowed(ltgp_engine* e, Shard& s) {
     CK(cudaSetDevice(s.dev));
-    const uint32_t nch = s.last_chunks;
-    std::vector<ChunkHdr> hdr(nch);
-    CK(cudaMemcpyAsync(hdr.data(), s.hdr.p, sizeof(ChunkHdr) * nch, cudaMemcpyDeviceToHost, s.st));
+    const uint32_t n = s.h_counters.as<uint32_t>()[2];
+    std::vector<uint32_t> idx(n);
+    CK(cudaMemcpyAsync(idx.data(), s.ovf.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, s.st));
     CK(cudaStreamSynchronize(s.st));
-    std::vector<Item> items;
-    std::vector<uint32_t> slots;
-    const Item* all = s.h_items.as<Item>();  // chunk items come first, in chunk order
-    for (uint32_t c = 0; c < nch; ++c)
-        if (hdr[c].flags & 1u) {
-            items.push_back(all[c]);
-            slots.push_back((uint32_t)slots.size());
-        }
-    const uint32_t n = (uint32_t)items.size();
-    if (n == 0) return 0;
-    const uint32_t cap = e->chunk / 2 + 2;  // a chunk holds at most C/2+1 leaves / C/2 ops
-    TRY(s.big_steps.ensure((size_t)n * cap, s.dev));
-    TRY(s.big_frames.ensure((size_t)n * cap * kFrameBytes, s.dev));
+    std::sort(idx.begin(), idx.end());
+    std::vector<Item> items(n);
+    std::vector<uint32_t> slots(n);
+    const Item* all = s.h_items.as<Item>();
+    for (uint32_t k = 0; k < n; ++k) {
+        items[k] = all[idx[k]];
+        slots[k] = k;
+    }
+    const uint32_t C = e->chunk;
+    const uint32_t fcap = C + 2, scap = C;
+    TRY(s.big_steps.ensure((size_t)n * scap, s.dev));
+    TRY(s.big_frames.ensure((size_t)n * fcap * kFrameBytes, s.dev));
+    const int grid = std::max(1, std::min<int>(kRerunCtas, (int)((n + kWarps - 1) / kWarps)));
+    TRY(s.big_spill.ensure((size_t)grid * kWarps * (C + 8) * kFrameBytes, s.dev));
     TRY(s.rerun_items.ensure(sizeof(Item) * n, s.dev));
     TRY(s.rerun_slot.ensure(sizeof(uint32_t) * n, s.dev));
     CK(cudaMemcpyAsync(s.rerun_items.p, items.data(), sizeof(Item) * n, cudaMemcpyHostToDevice, s.st));
@@ -359,14 +364,17 @@ int rerun_overflowed(ltgp_engine* e, Shard& s) {
     a.slot = s.rerun_slot.as<uint32_t>();
     a.steps = s.big_steps.as<uint8_t>();
     a.frames = s.big_frames.as<float2>();
-    a.max_steps = cap;
-    a.max_frames = cap;
-    const int grid = std::min<int>(s.eval_grid, (int)n);
-    K_EVAL<<<std::max(grid, 1), kWarps * 32, eval_smem_bytes(), s.st>>>(a, e->suite);
+    a.max_steps = scap;
+    a.max_frames = fcap;
+    a.spill = s.big_spill.as<float2>();
+    a.spill_frames = C + 8;
+    K_EVAL<<<grid, kWarps * 32, eval_smem_bytes(), s.st>>>(a, e->suite);
     CK(cudaGetLastError());
-    const int blocks = (int)std::min<uint32_t>((s.last_ctrees + 3) / 4, (uint32_t)s.sms * 16);
-    k_combine<<<blocks, 128, 0, s.st>>>(s.cargs, e->suite);
-    CK(cudaGetLastError());
+    if (s.last_ctrees) {
+        const int blocks = (int)std::min<uint32_t>((s.last_ctrees + 3) / 4, (uint32_t)s.sms * 16);
+        k_combine<<<blocks, 128, 0, s.st>>>(s.cargs, e->suite);
+        CK(cudaGetLastError());
+    }
     CK(cudaMemcpyAsync(s.h_counters.p, s.counters.p, 64, cudaMemcpyDeviceToHost, s.st));
     CK(cudaStreamSynchronize(s.st));
     s.last_reruns = n;
@@ -377,7 +385,7 @@ int rerun_overflowed(ltgp_engine* e, Shard& s) {
 int check_eval(Shard& s) {
     const uint32_t* c = s.h_counters.as<uint32_t>();
     if (c[2] != 0 || (c[1] & 1u)) {
-        set_err("chunk summary overflow in %u chunks", c[2]);
+        set_err("stack / chunk summary overflow in %u items after the worst-case re-run", c[2]);
         return -1;
     }
     if (c[1] & 8u) { set_err("k_eval shared-memory layout does not fit"); return -1; }

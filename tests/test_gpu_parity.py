@@ -134,6 +134,24 @@ def test_adversarial(oracle, suite):
         check_population(oracle, suite, gs, chunk=chunk)
 
 
+def test_capacity_overflow_reruns(oracle, suite):
+    """Items whose stack outgrows the per-warp spill area (a 16001-node left
+    chain is one whole-tree item holding 8001 values; its 64-node chunks are
+    all leaves) are re-run with worst-case capacities, bit-exactly."""
+    gs = [np.array([ADD] * 8000 + [X] + [5 + 7] * 8000, np.uint8),
+          np.array([SUB] * 5000 + [X] + list(range(5, 255)) * 20 + [X], np.uint8)[:10001]]
+    gs[1] = np.array([SUB] * 5000 + [X] + [5 + (k % 250) for k in range(5000)], np.uint8)
+    for chunk in (0, 64, 4096):
+        with engine(suite, chunk=chunk) as e:
+            e.upload_population(gs)
+            rec, outs = e.evaluate_outputs()
+            assert e.stats()["last_fallback_items"] > 0
+        for k, g in enumerate(gs):
+            o, _ = oracle.eval_batch(g, suite[0], suite[2])
+            assert same_bits(outs[k], o)
+            assert rec["depth"][k] == oracle.depth(g)
+
+
 def test_subtree_extents(oracle, suite):
     genomes = [ltgp.remy_tree(7, 4001), ltgp.random_tree_of_size(8, 999), np.array([X], np.uint8)]
     with engine(suite) as e:
