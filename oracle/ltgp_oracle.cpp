@@ -276,7 +276,11 @@ uint64_t suite_seed(uint64_t s) { return splitmix64(s ^ 0x53554954ull); }
 // H/genome.hpp:59-64: prefix-order draws;
 // functions draw below(4); terminals draw 4+below(251) (X or a constant);
 // grow below the depth cap draws below(255), mapping 1:1 to opcodes.
-bool gen_node(Rng& rng, int d, int target, bool full, std::vector<uint8_t>& out, uint64_t cap) {
+// grow_mode 0: below the cap draw below(255) -> opcode.
+// grow_mode 1 (SPEC.md:148 open question, GPquick-style): below(2) picks
+// function (then below(4)) or terminal (then 4+below(251)) with equal odds.
+bool gen_node(Rng& rng, int d, int target, bool full, std::vector<uint8_t>& out, uint64_t cap,
+              int grow_mode = 0) {
     // iterative prefix construction with an explicit stack of node depths
     std::vector<int> todo{d};
     while (!todo.empty()) {
@@ -285,7 +289,8 @@ bool gen_node(Rng& rng, int d, int target, bool full, std::vector<uint8_t>& out,
         uint8_t op;
         if (dep >= target) op = (uint8_t)(4 + rng.below(251));
         else if (full) op = (uint8_t)rng.below(4);
-        else op = (uint8_t)rng.below(255);
+        else if (grow_mode == 0) op = (uint8_t)rng.below(255);
+        else op = rng.below(2) == 0 ? (uint8_t)rng.below(4) : (uint8_t)(4 + rng.below(251));
         out.push_back(op);
         if (out.size() > cap) return false;
         if (is_function(op)) {
@@ -299,14 +304,14 @@ bool gen_node(Rng& rng, int d, int target, bool full, std::vector<uint8_t>& out,
 // H/genome.hpp:66-69: depth = dmin + (i/2) %
 // (dmax-dmin+1); even i -> full, odd i -> grow.
 bool ramped(Rng& rng, uint32_t count, uint64_t cap, int dmin, int dmax,
-            std::vector<std::vector<uint8_t>>& pop) {
+            std::vector<std::vector<uint8_t>>& pop, int grow_mode = 0) {
     pop.clear();
     for (uint32_t i = 0; i < count; ++i) {
         int d = dmin + (int)((i / 2) % (uint32_t)(dmax - dmin + 1));
         bool full = (i % 2) == 0;
         if (full && ((1ull << d) - 1) > cap) return false;  // std::length_error
         std::vector<uint8_t> g;
-        if (!gen_node(rng, 1, d, full, g, cap)) return false;
+        if (!gen_node(rng, 1, d, full, g, cap, grow_mode)) return false;
         pop.push_back(std::move(g));
     }
     return true;
@@ -554,7 +559,7 @@ void orc_plan_generation(uint64_t seed, uint32_t M, const orc_record* pop, uint3
 // splice + evaluate into fixed child slots) until max_generations or the
 // first child reaching node_limit.
 int64_t orc_run(uint32_t M, uint32_t G, uint64_t node_limit, uint32_t k, uint64_t seed,
-                int threads, const char* dump_path, int* reason, uint64_t* nodes_evaluated) {
+                int threads, const char* dump_path, int* reason, uint64_t* nodes_evaluated, int grow_mode) {
     Suite s;
     Rng srng(suite_seed(seed));
     make_suite(srng, s.in, s.tg, s.cs);
@@ -562,7 +567,7 @@ int64_t orc_run(uint32_t M, uint32_t G, uint64_t node_limit, uint32_t k, uint64_
     std::vector<std::vector<uint8_t>> pop, next(M);
     *reason = 0;
     *nodes_evaluated = 0;
-    if (!ramped(rng, M, node_limit, 2, 6, pop)) return -1;
+    if (!ramped(rng, M, node_limit, 2, 6, pop, grow_mode)) return -1;
     std::vector<orc_record> rec(M), nrec(M);
     FILE* dump = dump_path ? std::fopen(dump_path, "w") : nullptr;
     auto write_dump = [&](uint32_t gen) {

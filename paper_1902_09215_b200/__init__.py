@@ -88,7 +88,7 @@ _HOST_SIGS = {
     "ltgp_host_ramped": (C.c_uint64, [C.c_uint64, C.c_uint32, C.c_uint64, C.c_int, C.c_int, _P,
                                       C.c_uint64, _P]),
     "ltgp_host_plan_generation": (None, [C.c_uint64, C.c_uint32, _P, C.c_uint32, _P]),
-    "ltgp_host_run": (C.c_int64, [_P, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint64,
+    "ltgp_host_run": (C.c_int64, [_P, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint64, C.c_int,
                                   C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_uint64),
                                   C.POINTER(C.c_double)]),
 }
@@ -353,12 +353,12 @@ class Engine:
         return p.value, f.value, n.value, st.value
 
     def run(self, M: int, generations: int, node_limit: int, k: int = 7, seed: int = 1,
-            dump_path: str | None = None):
+            dump_path: str | None = None, grow_mode: int = 0):
         """run() (run.hpp:33-36) driven from C++ on this engine."""
         reason = C.c_int()
         nodes = C.c_uint64()
         secs = C.c_double()
-        done = host_lib().ltgp_host_run(self._h, M, generations, node_limit, k, seed,
+        done = host_lib().ltgp_host_run(self._h, M, generations, node_limit, k, seed, grow_mode,
                                         dump_path.encode() if dump_path else None,
                                         C.byref(reason), C.byref(nodes), C.byref(secs))
         if done < 0:

@@ -98,10 +98,17 @@ TestSuite make_suite(Rng& rng);              // sextic.hpp:50
 TestSuite make_suite(std::uint64_t seed);    // sextic.hpp:51
 std::uint64_t suite_seed(std::uint64_t run_seed);  // driver.hpp:17-19
 
+// Grow-method primitive choice below the depth cap: the SPEC's rule
+// (uniform over all 255 primitives) or the 50/50
+// function-vs-terminal alternative the SPEC leaves open.
+enum class GrowMode { kUniformPrimitive = 0, kHalfFunctions = 1 };
+
 Genome gen_full(Rng& rng, int target_depth, std::size_t capacity);   // genome.hpp:61
-Genome gen_grow(Rng& rng, int max_depth, std::size_t capacity);      // genome.hpp:64
+Genome gen_grow(Rng& rng, int max_depth, std::size_t capacity,
+                GrowMode mode = GrowMode::kUniformPrimitive);        // genome.hpp:64
 std::vector<Genome> ramped_half_and_half(Rng& rng, std::size_t count, std::size_t capacity,
-                                         int min_depth = 2, int max_depth = 6);  // genome.hpp:68
+                                         int min_depth = 2, int max_depth = 6,
+                                         GrowMode mode = GrowMode::kUniformPrimitive);  // genome.hpp:68
 Genome random_tree_of_size(Rng& rng, std::size_t nodes);             // bench.hpp:15
 void random_tree_of_size(Rng& rng, std::size_t nodes, std::uint8_t* out);
 

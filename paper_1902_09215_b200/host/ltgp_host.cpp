@@ -80,8 +80,11 @@ std::uint64_t suite_seed(std::uint64_t run_seed) { return splitmix64(run_seed ^ 
 namespace {
 // Prefix-order construction shared by gen_full / gen_grow (genome.hpp:59-64,
 // SPEC.md:72-89): function draws below(4), terminal draws 4+below(251), a
-// grow node above the cap draws below(255) (one draw per opcode).
-Genome build(Rng& rng, int cap_depth, bool full, std::size_t capacity) {
+// grow node above the cap draws below(255) (one draw per opcode) with
+// GrowMode::kUniformPrimitive, or below(2) function-vs-
+// terminal first with GrowMode::kHalfFunctions (the alternative SPEC.md:148
+// leaves open; GPquick-style, and the one whose runs bloat like the paper's).
+Genome build(Rng& rng, int cap_depth, bool full, std::size_t capacity, GrowMode mode) {
     std::vector<std::uint8_t> ops;
     std::vector<int> todo{1};
     while (!todo.empty()) {
@@ -90,7 +93,9 @@ Genome build(Rng& rng, int cap_depth, bool full, std::size_t capacity) {
         std::uint8_t op;
         if (d >= cap_depth) op = static_cast<std::uint8_t>(4 + rng.below(251));
         else if (full) op = static_cast<std::uint8_t>(rng.below(4));
-        else op = static_cast<std::uint8_t>(rng.below(255));
+        else if (mode == GrowMode::kUniformPrimitive) op = static_cast<std::uint8_t>(rng.below(255));
+        else op = rng.below(2) == 0 ? static_cast<std::uint8_t>(rng.below(4))
+                                    : static_cast<std::uint8_t>(4 + rng.below(251));
         ops.push_back(op);
         if (ops.size() > capacity) throw std::length_error("tree exceeds capacity");
         if (is_function(op)) {
@@ -106,24 +111,24 @@ Genome gen_full(Rng& rng, int target_depth, std::size_t capacity) {
     if (target_depth < 1) throw std::invalid_argument("depth < 1");
     if (target_depth >= 64 || ((std::size_t{1} << target_depth) - 1) > capacity)
         throw std::length_error("full tree exceeds capacity");
-    return build(rng, target_depth, true, capacity);
+    return build(rng, target_depth, true, capacity, GrowMode::kUniformPrimitive);
 }
 
-Genome gen_grow(Rng& rng, int max_depth, std::size_t capacity) {
+Genome gen_grow(Rng& rng, int max_depth, std::size_t capacity, GrowMode mode) {
     if (max_depth < 1) throw std::invalid_argument("depth < 1");
-    return build(rng, max_depth, false, capacity);
+    return build(rng, max_depth, false, capacity, mode);
 }
 
 // genome.hpp:66-69: depth dmin + (i/2) % span, even i
 // full, odd i grow.
 std::vector<Genome> ramped_half_and_half(Rng& rng, std::size_t count, std::size_t capacity,
-                                         int min_depth, int max_depth) {
+                                         int min_depth, int max_depth, GrowMode mode) {
     std::vector<Genome> out;
     out.reserve(count);
     const std::size_t span = static_cast<std::size_t>(max_depth - min_depth + 1);
     for (std::size_t i = 0; i < count; ++i) {
         const int d = min_depth + static_cast<int>((i / 2) % span);
-        out.push_back((i % 2 == 0) ? gen_full(rng, d, capacity) : gen_grow(rng, d, capacity));
+        out.push_back((i % 2 == 0) ? gen_full(rng, d, capacity) : gen_grow(rng, d, capacity, mode));
     }
     return out;
 }
@@ -344,7 +349,7 @@ uint64_t ltgp_host_ramped(uint64_t seed, uint32_t count, uint64_t capacity, int 
                           uint64_t out_cap, uint64_t* sizes) {
     try {
         Rng rng(seed);
-        const auto pop = ramped_half_and_half(rng, count, capacity, dmin, dmax);
+        const auto pop = ramped_half_and_half(rng, count, capacity, dmin, dmax, GrowMode::kUniformPrimitive);
         uint64_t pos = 0;
         for (uint32_t i = 0; i < count; ++i) {
             if (pos + pop[i].size() > out_cap) return 0;
@@ -371,7 +376,7 @@ void ltgp_host_plan_generation(uint64_t seed, uint32_t M, const ltgp_record* rec
 
 // run.hpp:33-36 on the engine.
 int64_t ltgp_host_run(ltgp_engine* e, uint32_t M, uint32_t G, uint64_t node_limit, uint32_t k, uint64_t seed,
-                      const char* dump_path, int* reason, uint64_t* nodes, double* eval_seconds) {
+                      int grow_mode, const char* dump_path, int* reason, uint64_t* nodes, double* eval_seconds) {
     try {
         RunConfig cfg;
         cfg.population_size = M;
@@ -383,7 +388,7 @@ int64_t ltgp_host_run(ltgp_engine* e, uint32_t M, uint32_t G, uint64_t node_limi
         const TestSuite suite = make_suite(suite_seed(seed));
         Rng rng(seed);
         std::vector<Individual> pop(M), next;
-        auto genomes = ramped_half_and_half(rng, M, node_limit, 2, 6);
+        auto genomes = ramped_half_and_half(rng, M, node_limit, 2, 6, static_cast<GrowMode>(grow_mode));
         for (uint32_t i = 0; i < M; ++i) pop[i].genome = std::move(genomes[i]);
         std::vector<WorkerState> pool(1);
         MemoryGauge gauge;

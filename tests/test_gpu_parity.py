@@ -207,17 +207,17 @@ def test_execute_generation_size_limit(suite):
         assert np.array_equal(e.download_genome(0), genomes[0])  # population unchanged
 
 
-@pytest.mark.parametrize("seed", [1, 2, 3])
-def test_run_dump_matches_oracle(oracle, tmp_path, seed):
+@pytest.mark.parametrize("seed,grow", [(1, 0), (2, 0), (3, 0), (1, 1), (2, 1)])
+def test_run_dump_matches_oracle(oracle, tmp_path, seed, grow):
     """run() on the engine vs the oracle's run(): identical generation dumps
     (fitness bits, hits, size, depth of every individual, every generation),
-    so selected parents are identical too."""
+    so selected parents are identical too. grow=1 runs bloat."""
     d_ref = tmp_path / "ref.txt"
-    r = oracle.run(48, 40, 10**9, 7, seed, 0, str(d_ref))
+    r = oracle.run(48, 40, 10**9, 7, seed, 0, str(d_ref), grow)
     for devices in ((0,), (0, 0)):
         d = tmp_path / f"gpu{len(devices)}.txt"
         with ltgp.Engine(list(devices), node_limit=10**9, chunk_nodes=256) as e:
-            g = e.run(48, 40, 10**9, 7, seed, str(d))
+            g = e.run(48, 40, 10**9, 7, seed, str(d), grow)
         assert g["generations"] == r["generations"] == 40
         assert d.read_bytes() == d_ref.read_bytes()
 
@@ -226,7 +226,7 @@ def test_run_size_limit_matches_oracle(oracle, tmp_path):
     # node_limit=63 -> SizeLimitHit within a few generations
     r = oracle.run(48, 300, 63, 7, 4, 0, str(tmp_path / "a"))
     with ltgp.Engine([0], node_limit=63) as e:
-        g = e.run(48, 300, 63, 7, 4, str(tmp_path / "b"))
+        g = e.run(48, 300, 63, 7, 4, str(tmp_path / "b"), 0)
     assert r["reason"] == g["reason"] == 1
     assert r["generations"] == g["generations"]
     assert (tmp_path / "a").read_bytes() == (tmp_path / "b").read_bytes()
@@ -243,3 +243,15 @@ def test_config3_full_size_sampled(oracle, suite):
     assert rec.tobytes() == rec2.tobytes()  # determinism across launches
     exp = oracle.evaluate_population(buf, offs, sizes, suite, threads=0)
     assert_records_equal(rec, exp)
+
+
+@pytest.mark.slow
+def test_config2_bloating_run_matches_oracle(oracle, tmp_path):
+    """Config 2 scale: pop 4000, tournament 7, no size limit, 100 generations
+    with the bloating grow variant; 2 shards; dumps identical to the oracle."""
+    r = oracle.run(4000, 100, 2**62, 7, 1, 0, str(tmp_path / "a"), 1)
+    with ltgp.Engine([0, 0], node_limit=2**62) as e:
+        g = e.run(4000, 100, 2**62, 7, 1, str(tmp_path / "b"), 1)
+    assert r["generations"] == g["generations"] == 100
+    assert r["nodes"] == g["nodes"]
+    assert (tmp_path / "a").read_bytes() == (tmp_path / "b").read_bytes()

@@ -257,7 +257,7 @@ def test_run_determinism_thread_invariance(oracle, tmp_path):
         dumps = []
         for threads in (1, 2, 8):
             p = tmp_path / f"d{seed}_{threads}.txt"
-            r = oracle.run(48, 15, 10**9, 7, seed, threads, str(p))
+            r = oracle.run(48, 15, 10**9, 7, seed, threads, str(p), 1)
             assert r["generations"] == 15
             dumps.append(p.read_bytes())
         assert dumps[0] == dumps[1] == dumps[2]
