@@ -64,7 +64,9 @@ typedef struct {
     double gather_seconds;      /* device time of the last record all-gather */
     uint64_t arena_high_water;  /* bytes, max over shards */
     uint64_t last_chunks;       /* chunk work items of the last evaluation */
-    uint64_t last_fallback_items; /* items re-run on the deep-stack path */
+    uint64_t last_fallback_items; /* items re-run with worst-case capacities */
+    uint64_t last_exits;        /* packets the fast path handed to the checked / window path */
+    uint64_t last_window_adjusts; /* of which needed a stack window spill or refill */
     uint32_t kernel_launches;   /* engine kernels launched by the last call */
 } ltgp_stats;
 

@@ -9,7 +9,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -34,6 +36,19 @@ constexpr uint32_t kSpillFrames = 1024;  // per warp; items that need more are r
 constexpr int kRerunCtas = 8;
 
 thread_local std::string g_err;
+
+// LTGP_TRACE=1: per-phase host wall times of execute_generation on stderr.
+struct Trace {
+    bool on = std::getenv("LTGP_TRACE") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    void mark(const char* what) {
+        if (!on) return;
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[ltgp] %-12s %8.1f us\n", what,
+                     std::chrono::duration<double, std::micro>(t - t0).count());
+        t0 = t;
+    }
+};
 
 void set_err(const char* fmt, ...) {
     char buf[1024];
@@ -65,9 +80,11 @@ struct DevBuf {
     int dev = -1;
     int ensure(size_t need, int device) {
         if (need <= bytes && p) return 0;
+        const size_t old = bytes;
         if (p) { cudaSetDevice(dev); cudaFree(p); p = nullptr; bytes = 0; }
-        size_t nb = std::max<size_t>(need, 256);
-        nb = nb + nb / 8;  // headroom against frequent regrowth
+        // geometric growth: bloating populations regrow O(log) times, and a
+        // regrow costs a device synchronisation (cudaFree)
+        size_t nb = std::max<size_t>({need + need / 8, 2 * old, size_t(256)});
         cudaSetDevice(device);
         cudaError_t e = cudaMalloc(&p, nb);
         if (e != cudaSuccess) {
@@ -455,7 +472,7 @@ int upload_tables(Shard& s, TreeSet& ts) {
 
 int collect(ltgp_engine* e, ltgp_record* out, float* outs48) {
     double secs = 0.0, ksecs = 0.0, csecs = 0.0;
-    uint64_t nodes = 0, chunks = 0, reruns = 0;
+    uint64_t nodes = 0, chunks = 0, reruns = 0, exits = 0, adjusts = 0;
     for (Shard& s : e->shards) {
         if (!s.count) continue;
         CK(cudaSetDevice(s.dev));
@@ -477,7 +494,11 @@ int collect(ltgp_engine* e, ltgp_record* out, float* outs48) {
         for (uint32_t i = 0; i < ts.count; ++i) nodes += ts.h_size[i];
         chunks += s.last_chunks;
         reruns += s.last_reruns;
+        exits += s.h_counters.as<uint32_t>()[4];
+        adjusts += s.h_counters.as<uint32_t>()[5];
     }
+    e->stats.last_exits = exits;
+    e->stats.last_window_adjusts = adjusts;
     e->stats.last_fallback_items = reruns;
     e->stats.eval_seconds = secs;
     e->stats.eval_kernel_seconds = ksecs;
@@ -757,6 +778,7 @@ int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M, 
             set_err("plan %u references slot outside the population", c);
             return -1;
         }
+    Trace tr;
     std::vector<DirEntry> dir;
     build_directory(e, dir);
     for (uint32_t c = 0; c < M; ++c)
@@ -801,6 +823,7 @@ int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M, 
         CK(cudaStreamSynchronize(s.st));
         if (qcount[g] && s.h_counters.as<uint32_t>()[3]) { set_err("malformed parent genome in extent scan"); return -1; }
     }
+    tr.mark("extents");
     // 2. SizeLimitHit (genome.hpp:71-84): child >= node_limit
     for (uint32_t c = 0; c < M; ++c)
         if (csize[c] >= e->cfg.node_limit || csize[c] > 0xffffffffull) { *size_limit_hit = 1; return 0; }
@@ -849,9 +872,13 @@ int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M, 
     }
     for (int g = 0; g < G; ++g) e->shards[g].cur = 1 - old_cur[g];
     e->stats.splice_seconds = splice_ms * 1e-3;
+    tr.mark("splice");
     // 4. evaluate the children
     TRY(ltgp_evaluate_launch(e));
-    return ltgp_evaluate_collect(e, out, nullptr);
+    tr.mark("eval launch");
+    TRY(ltgp_evaluate_collect(e, out, nullptr));
+    tr.mark("eval collect");
+    return 0;
 }
 
 int ltgp_subtree_extents(ltgp_engine* e, uint32_t count, const uint32_t* slots, const uint32_t* points,
