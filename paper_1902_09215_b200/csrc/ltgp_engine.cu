@@ -157,6 +157,7 @@ struct Shard {
     uint32_t last_reruns = 0;
     HostBuf h_items, h_ctrees, h_counters;
     uint32_t last_items = 0, last_chunks = 0, last_ctrees = 0;
+    uint32_t cur_chunk = kDefaultChunk, cur_max_frames = kMaxFrames, cur_max_steps = kMaxSteps;
     EvalArgs eargs;      // arguments of the last evaluation (for overflow reruns)
     CombineArgs cargs;
     const TreeSet* items_for = nullptr;  // work list cache: (set, version)
@@ -181,6 +182,7 @@ struct Shard {
 struct ltgp_engine {
     ltgp_config cfg;
     uint32_t chunk = kDefaultChunk;
+    bool chunk_fixed = false;  // chunk_nodes given in the config
     std::vector<Shard> shards;
     SuiteArgs suite;
     bool have_suite = false;
@@ -223,10 +225,23 @@ int init_shard(ltgp_engine* e, Shard& s) {
 // outputs) land in rec/outs. Asynchronous on s.st.
 int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     CK(cudaSetDevice(s.dev));
-    const uint32_t C = e->chunk;
     // --- work list (host): chunk items of large trees, then whole trees by
     // size. Cached while the tree set's layout is unchanged.
     if (s.items_for != &ts || s.items_version != ts.version) {
+        // chunk length: the configured one, or sized so the persistent grid
+        // gets >= ~8 items per warp (small populations must not wait on one
+        // warp per tree), between 256 and 16384 nodes
+        uint32_t C = e->chunk;
+        if (!e->chunk_fixed) {
+            uint64_t total = 0;
+            for (uint32_t t = 0; t < ts.count; ++t) total += ts.h_size[t];
+            const uint64_t per = total / ((uint64_t)s.eval_grid * kWarps * 8 + 1);
+            C = 256;
+            while (C < kDefaultChunk && (uint64_t)C * 2 <= per) C *= 2;
+        }
+        s.cur_chunk = C;
+        s.cur_max_frames = std::min<uint32_t>(kMaxFrames, std::max<uint32_t>(64, C / 4));
+        s.cur_max_steps = std::min<uint32_t>(kMaxSteps, C);
         std::vector<Item> chunks, whole;
         std::vector<CombineTree> ctrees;
         uint32_t nch = 0;
@@ -260,8 +275,8 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             CK(cudaMemcpyAsync(s.ctrees.p, s.h_ctrees.p, sizeof(CombineTree) * nct,
                                cudaMemcpyHostToDevice, s.st));
             TRY(s.hdr.ensure(sizeof(ChunkHdr) * nch, s.dev));
-            TRY(s.steps.ensure((size_t)kMaxSteps * nch, s.dev));
-            TRY(s.frames.ensure((size_t)kMaxFrames * kFrameBytes * nch, s.dev));
+            TRY(s.steps.ensure((size_t)s.cur_max_steps * nch, s.dev));
+            TRY(s.frames.ensure((size_t)s.cur_max_frames * kFrameBytes * nch, s.dev));
             TRY(s.dframes.ensure((size_t)kFrameBytes * nch, s.dev));
             TRY(s.segs.ensure(sizeof(Seg) * 2 * nch, s.dev));
         }
@@ -286,8 +301,8 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     a.hdr = s.hdr.as<ChunkHdr>();
     a.steps = s.steps.as<uint8_t>();
     a.frames = s.frames.as<float2>();
-    a.max_steps = kMaxSteps;
-    a.max_frames = kMaxFrames;
+    a.max_steps = s.cur_max_steps;
+    a.max_frames = s.cur_max_frames;
     a.spill = s.spill.as<float2>();
     a.spill_frames = kSpillFrames;
     TRY(s.ovf.ensure(sizeof(uint32_t) * std::max<uint32_t>(nitems, 1), s.dev));
@@ -364,7 +379,7 @@ int rerun_overflowed(ltgp_engine* e, Shard& s) {
         items[k] = all[idx[k]];
         slots[k] = k;
     }
-    const uint32_t C = e->chunk;
+    const uint32_t C = s.cur_chunk;
     const uint32_t fcap = C + 2, scap = C;
     TRY(s.big_steps.ensure((size_t)n * scap, s.dev));
     TRY(s.big_frames.ensure((size_t)n * fcap * kFrameBytes, s.dev));
@@ -530,6 +545,7 @@ int ltgp_engine_create(const ltgp_config* cfg, ltgp_engine** out) {
     if (cfg->chunk_nodes) {
         if (cfg->chunk_nodes % 16 || cfg->chunk_nodes < 64) { set_err("chunk_nodes must be a multiple of 16 >= 64"); return -1; }
         e->chunk = cfg->chunk_nodes;
+        e->chunk_fixed = true;
     }
     std::memset(&e->stats, 0, sizeof e->stats);
     e->shards.resize(cfg->n_shards);
