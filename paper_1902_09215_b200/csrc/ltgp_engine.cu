@@ -229,18 +229,18 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     // size. Cached while the tree set's layout is unchanged.
     if (s.items_for != &ts || s.items_version != ts.version) {
         // chunk length: the configured one, or sized so the persistent grid
-        // gets >= ~8 items per warp (small populations must not wait on one
-        // warp per tree), between 256 and 16384 nodes
+        // gets >= ~2 items per warp (small populations must not wait on one
+        // warp per tree; more chunks cost combine work), 1024..16384 nodes
         uint32_t C = e->chunk;
         if (!e->chunk_fixed) {
             uint64_t total = 0;
             for (uint32_t t = 0; t < ts.count; ++t) total += ts.h_size[t];
-            const uint64_t per = total / ((uint64_t)s.eval_grid * kWarps * 8 + 1);
-            C = 256;
+            const uint64_t per = total / ((uint64_t)s.eval_grid * kWarps * 2 + 1);
+            C = 1024;
             while (C < kDefaultChunk && (uint64_t)C * 2 <= per) C *= 2;
         }
         s.cur_chunk = C;
-        s.cur_max_frames = std::min<uint32_t>(kMaxFrames, std::max<uint32_t>(64, C / 4));
+        s.cur_max_frames = kMaxFrames;
         s.cur_max_steps = std::min<uint32_t>(kMaxSteps, C);
         std::vector<Item> chunks, whole;
         std::vector<CombineTree> ctrees;
