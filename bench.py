@@ -274,6 +274,20 @@ def run_ours(args, rank, world, local_rank):
                      "combine_ms": float(np.mean(comb)) * 1e3},
         "clocks": clk,
     }
+    if world == 1 and rank == 0 and not args.no_evolution:
+        # secondary: BASELINE configs[1] (pop 4000, k=7, crossover only, no size
+        # limit, 200 generations, bloating 50/50-grow variant — see DESIGN.md
+        # §6), run by the C++ host loop with splice + evaluation on the device
+        e.close()
+        with ltgp.Engine([local_rank], node_limit=2**62) as ev:
+            t0 = time.perf_counter()
+            r = ev.run(4000, 200, 2**62, 7, SEED, None, 1)
+            wall = time.perf_counter() - t0
+        line["evolution_c2"] = {
+            "generations": r["generations"], "nodes": r["nodes"],
+            "eval_gpops_per_s": r["nodes"] * LANES / max(r["eval_seconds"], 1e-12),
+            "e2e_gpops_per_s": r["nodes"] * LANES / wall, "wall_s": wall,
+            "note": "per-generation device evaluation (splice excluded) and whole-run wall clock incl. host planning"}
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         o, s2, cb, co, cs, ntrees = oracle_sample(threads, args.cpu_seconds)
@@ -297,6 +311,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-evolution", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
