@@ -68,6 +68,19 @@ void set_err(const char* fmt, ...) {
         }                                                                                 \
     } while (0)
 
+// LTGP_DEBUG_SYNC=1: synchronize after every launch so a fault names its kernel.
+static const bool g_debug_sync = std::getenv("LTGP_DEBUG_SYNC") != nullptr;
+#define DEBUG_SYNC(st, what)                                                                  \
+    do {                                                                                      \
+        if (g_debug_sync) {                                                                   \
+            cudaError_t _e = cudaStreamSynchronize(st);                                       \
+            if (_e != cudaSuccess) {                                                          \
+                set_err("%s failed: %s", what, cudaGetErrorString(_e));                       \
+                return -1;                                                                    \
+            }                                                                                 \
+        }                                                                                     \
+    } while (0)
+
 #define TRY(x)                  \
     do {                        \
         if ((x) != 0) return -1; \
@@ -195,6 +208,11 @@ namespace {
 
 static_assert(EvalLayout<kWarps, kWindow>::kBytes <= 227u * 1024u, "k_eval needs more than 227 KB of shared memory");
 size_t eval_smem_bytes() { return EvalLayout<kWarps, kWindow>::kBytes; }
+uint32_t spill_frames() {  // LTGP_SPILL_FRAMES overrides (debugging)
+    static const uint32_t v = std::getenv("LTGP_SPILL_FRAMES") ? (uint32_t)std::atoi(std::getenv("LTGP_SPILL_FRAMES"))
+                                                                : kSpillFrames;
+    return v;
+}
 #define K_EVAL k_eval<kWarps, kWindow>
 
 int init_shard(ltgp_engine* e, Shard& s) {
@@ -215,7 +233,7 @@ int init_shard(ltgp_engine* e, Shard& s) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K_EVAL, kWarps * 32, smem));
     if (per_sm < 1) { set_err("k_eval does not fit on an SM"); return -1; }
     s.eval_grid = per_sm * s.sms;
-    TRY(s.spill.ensure((size_t)s.eval_grid * kWarps * kSpillFrames * kFrameBytes, s.dev));
+    TRY(s.spill.ensure((size_t)s.eval_grid * kWarps * spill_frames() * kFrameBytes, s.dev));
     TRY(s.counters.ensure(64, s.dev));
     TRY(s.h_counters.ensure(64));
     return 0;
@@ -304,7 +322,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     a.max_steps = s.cur_max_steps;
     a.max_frames = s.cur_max_frames;
     a.spill = s.spill.as<float2>();
-    a.spill_frames = kSpillFrames;
+    a.spill_frames = spill_frames();
     TRY(s.ovf.ensure(sizeof(uint32_t) * std::max<uint32_t>(nitems, 1), s.dev));
     a.ovf = s.ovf.as<uint32_t>();
     a.rec = s.rec.as<float>();
@@ -333,18 +351,21 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         const uint64_t blocks = std::min<uint64_t>((packets + 255) / 256, (uint64_t)s.sms * 16);
         k_decode<<<(unsigned)blocks, 256, 0, s.st>>>(ts.arena.as<uint4>(), dec, packets);
         CK(cudaGetLastError());
+        DEBUG_SYNC(s.st, "k_decode");
         ++launches;
     }
     if (nitems) {
         k_plan<<<(nitems + 127) / 128, 128, 0, s.st>>>(s.items.as<Item>(), nitems, ts.off.as<uint64_t>(),
                                                       reinterpret_cast<uint8_t*>(dec), packets, kWindow);
         CK(cudaGetLastError());
+        DEBUG_SYNC(s.st, "k_plan");
         ++launches;
     }
     if (nitems) {
         const int grid = std::min<int>(s.eval_grid, (int)nitems);
         K_EVAL<<<std::max(grid, 1), kWarps * 32, eval_smem_bytes(), s.st>>>(a, e->suite);
         CK(cudaGetLastError());
+        DEBUG_SYNC(s.st, "k_eval");
         ++launches;
     }
     CK(cudaEventRecord(s.ev[4], s.st));
@@ -352,6 +373,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         const int blocks = (int)std::min<uint32_t>((nct + 3) / 4, (uint32_t)s.sms * 16);
         k_combine<<<blocks, 128, 0, s.st>>>(ca, e->suite);
         CK(cudaGetLastError());
+        DEBUG_SYNC(s.st, "k_combine");
         ++launches;
     }
     CK(cudaEventRecord(s.ev[1], s.st));
@@ -402,6 +424,7 @@ int rerun_overflowed(ltgp_engine* e, Shard& s) {
     a.spill_frames = C + 8;
     K_EVAL<<<grid, kWarps * 32, eval_smem_bytes(), s.st>>>(a, e->suite);
     CK(cudaGetLastError());
+    DEBUG_SYNC(s.st, "k_eval (re-run)");
     if (s.last_ctrees) {
         const int blocks = (int)std::min<uint32_t>((s.last_ctrees + 3) / 4, (uint32_t)s.sms * 16);
         k_combine<<<blocks, 128, 0, s.st>>>(s.cargs, e->suite);

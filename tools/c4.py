@@ -1,0 +1,50 @@
+"""Config 4 at configurable scale: T uniform-random (Remy) trees of N nodes,
+evaluated as one population; checks `--check` trees against the oracle."""
+import argparse
+import os
+import sys
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1902_09215_b200 as ltgp  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--trees", type=int, default=48)
+    ap.add_argument("--nodes", type=int, default=10_000_001)
+    ap.add_argument("--check", type=int, default=2)
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--chunk", type=int, default=0)
+    a = ap.parse_args()
+    n = a.nodes | 1
+    t = time.perf_counter()
+    with ThreadPoolExecutor(os.cpu_count()) as ex:
+        trees = list(ex.map(lambda i: ltgp.remy_tree(7000 + i, n), range(a.trees)))
+    print(f"generated {a.trees} x {n} nodes in {time.perf_counter() - t:.1f} s", flush=True)
+    suite = ltgp.make_suite(ltgp.suite_seed(1))
+    with ltgp.Engine([0], node_limit=2**62, chunk_nodes=a.chunk) as e:
+        e.set_suite(*suite)
+        e.upload_population(trees)
+        for _ in range(a.reps):
+            rec, outs = e.evaluate_outputs()
+            st = e.stats()
+            tot = a.trees * n
+            print(f"eval {st['eval_seconds']*1e3:.1f} ms (k_eval {st['eval_kernel_seconds']*1e3:.1f}, combine "
+                  f"{st['combine_seconds']*1e3:.1f}) {tot*48/st['eval_seconds']/1e12:.3f} T GPops/s, chunks "
+                  f"{st['last_chunks']}, reruns {st['last_fallback_items']}, exits {st['last_exits']}, "
+                  f"adjusts {st['last_window_adjusts']}", flush=True)
+    if a.check:
+        from tests._oracle import load_oracle, same_bits
+        o = load_oracle()
+        for k in range(a.check):
+            out, _ = o.eval_batch(trees[k], suite[0], suite[2])
+            ok = same_bits(outs[k], out) and rec["depth"][k] == o.depth(trees[k])
+            print(f"tree {k}: depth {rec['depth'][k]}, matches oracle: {ok}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
