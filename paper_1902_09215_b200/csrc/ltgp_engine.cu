@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <cstdarg>
 #include <cstdlib>
@@ -32,6 +33,8 @@ constexpr int kWindow = 25;          // shared stack window frames per warp
 constexpr uint32_t kDefaultChunk = 16384;
 constexpr uint32_t kMaxSteps = 1024;
 constexpr uint32_t kMaxFrames = 256;
+constexpr uint32_t kMaxChunk = 65536;      // automatic chunk length ceiling
+constexpr uint64_t kCombineChunks = 128;   // target chunks per tree (sequential combine)
 constexpr uint32_t kSpillFrames = 1024;  // per warp; items that need more are re-run
 constexpr int kRerunCtas = 8;
 
@@ -156,7 +159,7 @@ uint64_t g_version = 0;
 struct Shard {
     int dev = 0;
     cudaStream_t st = nullptr;
-    cudaEvent_t ev[6] = {};
+    cudaEvent_t ev[8] = {};
     int sms = 0;
     int eval_grid = 0;
     uint32_t first = 0, count = 0;  // global slot range
@@ -165,7 +168,8 @@ struct Shard {
     TreeSet scratch;                // ltgp_eval_one
     // evaluation scratch
     DevBuf items, ctrees, hdr, steps, frames, dframes, segs, spill, counters, rec, outs;
-    DevBuf big_steps, big_frames, rerun_items, rerun_slot, ovf, big_spill;  // overflow reruns
+    DevBuf big_steps[2], big_frames[2], rerun_items[2], rerun_slot[2], ovf, big_spill;  // overflow re-runs (2 tiers)
+    double rerun_ksecs = 0.0, rerun_csecs = 0.0;
     bool last_outs = false;
     uint32_t last_reruns = 0;
     HostBuf h_items, h_ctrees, h_counters;
@@ -181,8 +185,9 @@ struct Shard {
     void release() {
         set[0].release(); set[1].release(); scratch.release();
         for (DevBuf* b : {&items, &ctrees, &hdr, &steps, &frames, &dframes, &segs, &spill, &counters,
-                          &rec, &outs, &plans, &ext, &csize, &coff, &dir, &big_steps, &big_frames,
-                          &rerun_items, &rerun_slot, &ovf, &big_spill}) b->release();
+                          &rec, &outs, &plans, &ext, &csize, &coff, &dir, &big_steps[0], &big_frames[0],
+                          &big_steps[1], &big_frames[1], &rerun_items[0], &rerun_slot[0], &rerun_items[1],
+                          &rerun_slot[1], &ovf, &big_spill}) b->release();
         h_items.release(); h_ctrees.release(); h_counters.release();
         h_csize.release(); h_coff.release(); h_dir.release();
         if (st) { cudaSetDevice(dev); cudaStreamDestroy(st); }
@@ -248,18 +253,29 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     if (s.items_for != &ts || s.items_version != ts.version) {
         // chunk length: the configured one, or sized so the persistent grid
         // gets >= ~2 items per warp (small populations must not wait on one
-        // warp per tree; more chunks cost combine work), 1024..16384 nodes
+        // warp per tree; more chunks cost combine work), 1024..16384 nodes;
+        // and long enough that the largest tree has
+        // at most kCombineChunks chunks, up to kMaxChunk, since k_combine
+        // replays one tree's chunks sequentially (a lone huge tree)
         uint32_t C = e->chunk;
         if (!e->chunk_fixed) {
-            uint64_t total = 0;
-            for (uint32_t t = 0; t < ts.count; ++t) total += ts.h_size[t];
+            uint64_t total = 0, biggest = 0;
+            for (uint32_t t = 0; t < ts.count; ++t) {
+                total += ts.h_size[t];
+                biggest = std::max<uint64_t>(biggest, ts.h_size[t]);
+            }
             const uint64_t per = total / ((uint64_t)s.eval_grid * kWarps * 2 + 1);
             C = 1024;
             while (C < kDefaultChunk && (uint64_t)C * 2 <= per) C *= 2;
+            while (C < kMaxChunk && (uint64_t)C * kCombineChunks < biggest) C *= 2;
         }
+        // summary capacities: a chunk's spine and its frames (K frames +
+        // outputs) grow like sqrt(C) (Remy-random trees: mean ~1.6 sqrt(C),
+        // max ~3.6 sqrt(C) frames, ~6 sqrt(C) steps)
+        const uint32_t rc = (uint32_t)std::lround(std::sqrt((double)C));
         s.cur_chunk = C;
-        s.cur_max_frames = kMaxFrames;
-        s.cur_max_steps = std::min<uint32_t>(kMaxSteps, C);
+        s.cur_max_frames = std::max<uint32_t>(kMaxFrames, (6 * rc + 63) & ~63u);
+        s.cur_max_steps = std::min<uint32_t>(C, std::max<uint32_t>(kMaxSteps, 16 * rc));
         std::vector<Item> chunks, whole;
         std::vector<CombineTree> ctrees;
         uint32_t nch = 0;
@@ -339,6 +355,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     ca.counters = s.counters.as<uint32_t>();
     s.last_outs = want_outs;
     s.last_reruns = 0;
+    s.rerun_ksecs = s.rerun_csecs = 0.0;
     const uint64_t packets = (ts.bytes + 15) / 16;
     // +1 KB: the fast path stages record groups up to 512 B past an item
     TRY(ts.decode.ensure(std::max<uint64_t>(packets, 1) * 32 + 1024, s.dev));
@@ -370,8 +387,8 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     }
     CK(cudaEventRecord(s.ev[4], s.st));
     if (nct) {
-        const int blocks = (int)std::min<uint32_t>((nct + 3) / 4, (uint32_t)s.sms * 16);
-        k_combine<<<blocks, 128, 0, s.st>>>(ca, e->suite);
+        const int blocks = (int)std::min<uint32_t>((nct + kCombineWarps - 1) / kCombineWarps, (uint32_t)s.sms * 16);
+        k_combine<<<blocks, kCombineWarps * 32, 0, s.st>>>(ca, e->suite);
         CK(cudaGetLastError());
         DEBUG_SYNC(s.st, "k_combine");
         ++launches;
@@ -383,68 +400,109 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
 }
 
 // Items whose stack outgrew the per-warp spill area, or chunks whose summary
-// outgrew the per-chunk capacity, are re-scanned with worst-case capacities
-// (a chunk of C nodes holds at most C stack values, C spine steps), on a
-// small grid with its own spill area; then every chunked tree is recombined.
-// Synchronous; only taken when the counters report an overflow.
+// outgrew the per-chunk capacity, are re-scanned in two tiers: first with 4x
+// the summary capacities on the full grid (a long-spined random tree
+// occasionally needs that), then whatever still overflows with worst-case
+// capacities (a chunk of C nodes holds at most C stack values, C spine steps)
+// on a small grid with its own spill area; then every chunked tree is
+// recombined once. Synchronous; only taken when the counters report an
+// overflow. Device time is added to the evaluation's.
 int rerun_overflowed(ltgp_engine* e, Shard& s) {
     CK(cudaSetDevice(s.dev));
-    const uint32_t n = s.h_counters.as<uint32_t>()[2];
-    std::vector<uint32_t> idx(n);
-    CK(cudaMemcpyAsync(idx.data(), s.ovf.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, s.st));
-    CK(cudaStreamSynchronize(s.st));
-    std::sort(idx.begin(), idx.end());
-    std::vector<Item> items(n);
-    std::vector<uint32_t> slots(n);
-    const Item* all = s.h_items.as<Item>();
-    for (uint32_t k = 0; k < n; ++k) {
-        items[k] = all[idx[k]];
-        slots[k] = k;
-    }
     const uint32_t C = s.cur_chunk;
-    const uint32_t fcap = C + 2, scap = C;
-    TRY(s.big_steps.ensure((size_t)n * scap, s.dev));
-    TRY(s.big_frames.ensure((size_t)n * fcap * kFrameBytes, s.dev));
-    const int grid = std::max(1, std::min<int>(kRerunCtas, (int)((n + kWarps - 1) / kWarps)));
-    TRY(s.big_spill.ensure((size_t)grid * kWarps * (C + 8) * kFrameBytes, s.dev));
-    TRY(s.rerun_items.ensure(sizeof(Item) * n, s.dev));
-    TRY(s.rerun_slot.ensure(sizeof(uint32_t) * n, s.dev));
-    CK(cudaMemcpyAsync(s.rerun_items.p, items.data(), sizeof(Item) * n, cudaMemcpyHostToDevice, s.st));
-    CK(cudaMemcpyAsync(s.rerun_slot.p, slots.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice, s.st));
-    CK(cudaMemsetAsync(s.counters.p, 0, 64, s.st));
-    EvalArgs a = s.eargs;
-    a.items = s.rerun_items.as<Item>();
-    a.n_items = n;
-    a.slot = s.rerun_slot.as<uint32_t>();
-    a.steps = s.big_steps.as<uint8_t>();
-    a.frames = s.big_frames.as<float2>();
-    a.max_steps = scap;
-    a.max_frames = fcap;
-    a.spill = s.big_spill.as<float2>();
-    a.spill_frames = C + 8;
-    K_EVAL<<<grid, kWarps * 32, eval_smem_bytes(), s.st>>>(a, e->suite);
-    CK(cudaGetLastError());
-    DEBUG_SYNC(s.st, "k_eval (re-run)");
-    if (s.last_ctrees) {
-        const int blocks = (int)std::min<uint32_t>((s.last_ctrees + 3) / 4, (uint32_t)s.sms * 16);
-        k_combine<<<blocks, 128, 0, s.st>>>(s.cargs, e->suite);
+    std::vector<Item> prev(s.h_items.as<Item>(), s.h_items.as<Item>() + s.last_items);
+    uint32_t total = 0;
+    float ms = 0.0f;
+    // k_eval's error flags other than "overflow" and the pass statistics
+    // survive the tiers (the first combine's verdict, [6], is superseded)
+    uint32_t* hc = s.h_counters.as<uint32_t>();
+    uint32_t keep = hc[1] & ~1u;
+    const uint32_t exits = hc[4], adjusts = hc[5];
+    for (int tier = 1; tier <= 2; ++tier) {
+        const uint32_t n = hc[2];
+        if (n == 0) break;
+        std::vector<uint32_t> idx(n);
+        CK(cudaMemcpyAsync(idx.data(), s.ovf.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, s.st));
+        CK(cudaStreamSynchronize(s.st));
+        std::sort(idx.begin(), idx.end());
+        std::vector<Item> items(n);
+        std::vector<uint32_t> slots(n);
+        for (uint32_t k = 0; k < n; ++k) {
+            items[k] = prev[idx[k]];
+            slots[k] = k;
+        }
+        if (tier == 1) total = n;
+        const bool worst = tier == 2;
+        const uint32_t fcap = worst ? C + 2 : std::min(C + 2, 4 * s.cur_max_frames);
+        const uint32_t scap = worst ? C : std::min(C, 4 * s.cur_max_steps);
+        DevBuf& bsteps = s.big_steps[tier - 1];
+        DevBuf& bframes = s.big_frames[tier - 1];
+        TRY(bsteps.ensure((size_t)n * scap, s.dev));
+        TRY(bframes.ensure((size_t)n * fcap * kFrameBytes, s.dev));
+        int grid;
+        EvalArgs a = s.eargs;
+        if (worst) {
+            grid = std::max(1, std::min<int>(kRerunCtas, (int)((n + kWarps - 1) / kWarps)));
+            TRY(s.big_spill.ensure((size_t)grid * kWarps * (C + 8) * kFrameBytes, s.dev));
+            a.spill = s.big_spill.as<float2>();
+            a.spill_frames = C + 8;
+        } else {
+            grid = std::max(1, std::min<int>(s.eval_grid, (int)((n + kWarps - 1) / kWarps)));
+        }
+        TRY(s.rerun_items[tier - 1].ensure(sizeof(Item) * n, s.dev));
+        TRY(s.rerun_slot[tier - 1].ensure(sizeof(uint32_t) * n, s.dev));
+        CK(cudaMemcpyAsync(s.rerun_items[tier - 1].p, items.data(), sizeof(Item) * n, cudaMemcpyHostToDevice, s.st));
+        CK(cudaMemcpyAsync(s.rerun_slot[tier - 1].p, slots.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice,
+                           s.st));
+        CK(cudaMemsetAsync(s.counters.p, 0, 64, s.st));
+        a.items = s.rerun_items[tier - 1].as<Item>();
+        a.n_items = n;
+        a.slot = s.rerun_slot[tier - 1].as<uint32_t>();
+        a.steps = bsteps.as<uint8_t>();
+        a.frames = bframes.as<float2>();
+        a.max_steps = scap;
+        a.max_frames = fcap;
+        CK(cudaEventRecord(s.ev[5], s.st));
+        K_EVAL<<<grid, kWarps * 32, eval_smem_bytes(), s.st>>>(a, e->suite);
         CK(cudaGetLastError());
+        DEBUG_SYNC(s.st, "k_eval (re-run)");
+        CK(cudaEventRecord(s.ev[6], s.st));
+        CK(cudaMemcpyAsync(s.h_counters.p, s.counters.p, 64, cudaMemcpyDeviceToHost, s.st));
+        CK(cudaStreamSynchronize(s.st));
+        CK(cudaEventElapsedTime(&ms, s.ev[5], s.ev[6]));
+        s.rerun_ksecs += ms * 1e-3;
+        e->stats.kernel_launches += 1;
+        if (tier == 1) keep |= hc[1] & ~1u;
+        prev.swap(items);
     }
-    CK(cudaMemcpyAsync(s.h_counters.p, s.counters.p, 64, cudaMemcpyDeviceToHost, s.st));
-    CK(cudaStreamSynchronize(s.st));
-    s.last_reruns = n;
-    e->stats.kernel_launches += 2;
+    if (s.last_ctrees) {
+        CK(cudaEventRecord(s.ev[5], s.st));
+        const int blocks = (int)std::min<uint32_t>((s.last_ctrees + kCombineWarps - 1) / kCombineWarps, (uint32_t)s.sms * 16);
+        k_combine<<<blocks, kCombineWarps * 32, 0, s.st>>>(s.cargs, e->suite);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(s.ev[6], s.st));
+        CK(cudaMemcpyAsync(s.h_counters.p, s.counters.p, 64, cudaMemcpyDeviceToHost, s.st));
+        CK(cudaStreamSynchronize(s.st));
+        CK(cudaEventElapsedTime(&ms, s.ev[5], s.ev[6]));
+        s.rerun_csecs += ms * 1e-3;
+        e->stats.kernel_launches += 1;
+    }
+    hc[1] |= keep;
+    hc[4] = exits;
+    hc[5] = adjusts;
+    s.last_reruns = total;
     return 0;
 }
 
 int check_eval(Shard& s) {
     const uint32_t* c = s.h_counters.as<uint32_t>();
-    if (c[2] != 0 || (c[1] & 1u)) {
+    const uint32_t flags = c[1] | c[6];  // k_eval's and k_combine's
+    if (c[2] != 0 || (flags & 1u)) {
         set_err("stack / chunk summary overflow in %u items after the worst-case re-run", c[2]);
         return -1;
     }
-    if (c[1] & 8u) { set_err("k_eval shared-memory layout does not fit"); return -1; }
-    if (c[1] & 2u) { set_err("malformed genome (stack underflow or leftover values)"); return -1; }
+    if (flags & 8u) { set_err("k_eval shared-memory layout does not fit"); return -1; }
+    if (flags & 2u) { set_err("malformed genome (stack underflow or leftover values)"); return -1; }
     return 0;
 }
 
@@ -522,12 +580,15 @@ int collect(ltgp_engine* e, ltgp_record* out, float* outs48) {
                                        sizeof(float) * kLanes * s.count, cudaMemcpyDeviceToHost, s.st));
         CK(cudaStreamSynchronize(s.st));
         float ms = 0.0f;
-        CK(cudaEventElapsedTime(&ms, s.ev[0], s.ev[1]));
-        secs = std::max(secs, ms * 1e-3);
+        // device time of the pass plus any overflow re-run (its k_eval tiers
+        // count as evaluation, its recombine replaces the first combine)
         CK(cudaEventElapsedTime(&ms, s.ev[0], s.ev[4]));
-        ksecs = std::max(ksecs, ms * 1e-3);
+        const double k = ms * 1e-3 + s.rerun_ksecs;
         CK(cudaEventElapsedTime(&ms, s.ev[4], s.ev[1]));
-        csecs = std::max(csecs, ms * 1e-3);
+        const double cmb = ms * 1e-3 + s.rerun_csecs;
+        secs = std::max(secs, k + cmb);
+        ksecs = std::max(ksecs, k);
+        csecs = std::max(csecs, cmb);
         const TreeSet& ts = s.set[s.cur];
         for (uint32_t i = 0; i < ts.count; ++i) nodes += ts.h_size[i];
         chunks += s.last_chunks;
