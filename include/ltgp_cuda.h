@@ -101,6 +101,16 @@ int ltgp_evaluate_population(ltgp_engine* e, ltgp_record* out, uint64_t* nodes);
    (eval_batch_raw's result frame, eval.hpp:73-74) into outs48[M*48]. */
 int ltgp_evaluate_outputs(ltgp_engine* e, ltgp_record* out, float* outs48);
 
+/* evaluate_population (evolve.hpp:108-109) on host genomes in one call:
+   the packed buffer (same layout rules as ltgp_upload_packed) becomes the
+   population and is evaluated while it uploads. Slices of ~32 MB go
+   host-to-device on a copy stream and each slice's trees are evaluated as
+   soon as they land. buf should be pinned (pageable memory works but
+   serialises the copy). out: M records; outs48: per-case outputs or NULL. */
+int ltgp_evaluate_packed(ltgp_engine* e, uint32_t M, const uint8_t* buf, uint64_t buf_bytes,
+                         const uint64_t* offsets, const uint64_t* sizes, ltgp_record* out,
+                         float* outs48);
+
 /* Same work, split in two halves so callers can time the device part
    alone: launch (async) then collect (waits, copies records). */
 int ltgp_evaluate_launch(ltgp_engine* e);

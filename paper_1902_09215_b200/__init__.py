@@ -64,6 +64,7 @@ _CUDA_SIGS = {
     "ltgp_set_suite": (C.c_int, [_P, _P, _P, _P]),
     "ltgp_upload_population": (C.c_int, [_P, C.c_uint32, _P, _P]),
     "ltgp_upload_packed": (C.c_int, [_P, C.c_uint32, _P, C.c_uint64, _P, _P]),
+    "ltgp_evaluate_packed": (C.c_int, [_P, C.c_uint32, _P, C.c_uint64, _P, _P, _P, _P]),
     "ltgp_evaluate_population": (C.c_int, [_P, _P, _P]),
     "ltgp_evaluate_outputs": (C.c_int, [_P, _P, _P]),
     "ltgp_evaluate_launch": (C.c_int, [_P]),
@@ -290,6 +291,22 @@ class Engine:
         sizes = np.ascontiguousarray(sizes, np.uint64)
         _check(self._lib.ltgp_upload_packed(self._h, len(sizes), _ptr(buf), buf.nbytes, _ptr(offsets),
                                             _ptr(sizes)))
+
+    def evaluate_packed(self, buf: np.ndarray, offsets: np.ndarray, sizes: np.ndarray, outputs: bool = False,
+                        rec: np.ndarray | None = None):
+        """evaluate_population on host genomes in one call: the packed buffer
+        becomes the population and is evaluated while it uploads (slices
+        overlap the copy; ``buf`` should be pinned). Returns records, or
+        (records, outputs[M, 48]) with ``outputs``."""
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        sizes = np.ascontiguousarray(sizes, np.uint64)
+        M = len(sizes)
+        if rec is None:
+            rec = np.zeros(M, RECORD_DTYPE)
+        outs = np.zeros((M, LANES), np.float32) if outputs else None
+        _check(self._lib.ltgp_evaluate_packed(self._h, M, _ptr(buf), buf.nbytes, _ptr(offsets), _ptr(sizes),
+                                              _ptr(rec), _ptr(outs)))
+        return (rec, outs) if outputs else rec
 
     def population_size(self) -> int:
         return int(self._lib.ltgp_population_size(self._h))

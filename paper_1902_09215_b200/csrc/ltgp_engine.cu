@@ -156,9 +156,28 @@ struct TreeSet {
 
 uint64_t g_version = 0;
 
+// Streamed evaluation: slice g = trees [tree_begin, next slice's) whose bytes
+// are host src[src, src+len) -> arena[dst, dst+len).
+struct Slice {
+    uint32_t tree_begin;
+    uint64_t src, dst, len;
+};
+constexpr uint32_t kMaxSlices = 16;
+constexpr uint64_t kSlicePad = 2048;   // arena gap between slices (k_eval's record look-ahead < 1 KB)
+constexpr uint64_t kSliceBytes = 32ull << 20;  // target bytes per slice
+constexpr uint32_t kQueueBase = 16;    // counters[16 + g]: work queue of slice g
+constexpr size_t kCounterBytes = 256;
+
 struct Shard {
     int dev = 0;
     cudaStream_t st = nullptr;
+    cudaStream_t st2 = nullptr, cst = nullptr;  // second compute stream, copy stream (streamed evaluation)
+    std::vector<cudaEvent_t> sev;               // 3 per slice: copied, planned, evaluated
+    std::vector<Slice> slices;                  // non-empty during a streamed evaluation
+    const uint8_t* src = nullptr;               // its pinned host source
+    std::vector<uint32_t> slice_items;          // slice g's items: [slice_items[g], slice_items[g+1])
+    std::vector<uint32_t> items_slices;         // work-list cache key (slice tree boundaries)
+    DevBuf spill2;                              // spill area of the second compute stream
     cudaEvent_t ev[8] = {};
     int sms = 0;
     int eval_grid = 0;
@@ -190,8 +209,12 @@ struct Shard {
                           &rerun_slot[1], &ovf, &big_spill}) b->release();
         h_items.release(); h_ctrees.release(); h_counters.release();
         h_csize.release(); h_coff.release(); h_dir.release();
+        spill2.release();
         if (st) { cudaSetDevice(dev); cudaStreamDestroy(st); }
+        if (st2) cudaStreamDestroy(st2);
+        if (cst) cudaStreamDestroy(cst);
         for (auto& e : ev) if (e) cudaEventDestroy(e);
+        for (auto& e : sev) if (e) cudaEventDestroy(e);
     }
 };
 
@@ -223,7 +246,11 @@ uint32_t spill_frames() {  // LTGP_SPILL_FRAMES overrides (debugging)
 int init_shard(ltgp_engine* e, Shard& s) {
     CK(cudaSetDevice(s.dev));
     CK(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&s.st2, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&s.cst, cudaStreamNonBlocking));
     for (auto& ev : s.ev) CK(cudaEventCreate(&ev));
+    s.sev.resize(3 * kMaxSlices);
+    for (auto& ev : s.sev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, s.dev));
     if (prop.major < 10) {
@@ -239,24 +266,37 @@ int init_shard(ltgp_engine* e, Shard& s) {
     if (per_sm < 1) { set_err("k_eval does not fit on an SM"); return -1; }
     s.eval_grid = per_sm * s.sms;
     TRY(s.spill.ensure((size_t)s.eval_grid * kWarps * spill_frames() * kFrameBytes, s.dev));
-    TRY(s.counters.ensure(64, s.dev));
+    TRY(s.counters.ensure(kCounterBytes, s.dev));
     TRY(s.h_counters.ensure(64));
     return 0;
 }
 
 // Evaluate every tree of `ts` on shard s: records (and optional per-case
 // outputs) land in rec/outs. Asynchronous on s.st.
+//
+// Streamed evaluation (s.slices non-empty, ltgp_evaluate_packed): the trees
+// arrive from pinned host memory in slices (consecutive trees, each slice
+// 2 KB apart in the arena). Slice g's bytes go over a copy stream; its
+// k_decode, k_plan and k_eval start as soon as they land, alternating between
+// two compute streams so one slice's k_eval fills the SMs the previous
+// slice's tail frees. The upload overlaps the evaluation. Without slices the
+// arena is resident and the whole set is one slice on s.st.
 int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     CK(cudaSetDevice(s.dev));
-    // --- work list (host): chunk items of large trees, then whole trees by
-    // size. Cached while the tree set's layout is unchanged.
-    if (s.items_for != &ts || s.items_version != ts.version) {
+    const bool streamed = !s.slices.empty();
+    const uint32_t G = streamed ? (uint32_t)s.slices.size() : 1u;
+    // --- work list (host), per slice: chunk items of large trees, then whole
+    // trees by size. Cached while the tree set's layout and slicing are unchanged.
+    std::vector<uint32_t> tb(G + 1);  // slice g = trees [tb[g], tb[g+1])
+    for (uint32_t g = 0; g < G; ++g) tb[g] = streamed ? s.slices[g].tree_begin : 0u;
+    tb[G] = ts.count;
+    if (s.items_for != &ts || s.items_version != ts.version || s.items_slices != tb) {
         // chunk length: the configured one, or sized so the persistent grid
         // gets >= ~2 items per warp (small populations must not wait on one
         // warp per tree; more chunks cost combine work), 1024..16384 nodes;
-        // and long enough that the largest tree has
-        // at most kCombineChunks chunks, up to kMaxChunk, since k_combine
-        // replays one tree's chunks sequentially (a lone huge tree)
+        // and long enough that the largest tree has at most kCombineChunks
+        // chunks, up to kMaxChunk, since k_combine replays one tree's chunks
+        // sequentially (a lone huge tree)
         uint32_t C = e->chunk;
         if (!e->chunk_fixed) {
             uint64_t total = 0, biggest = 0;
@@ -276,31 +316,36 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         s.cur_chunk = C;
         s.cur_max_frames = std::max<uint32_t>(kMaxFrames, (6 * rc + 63) & ~63u);
         s.cur_max_steps = std::min<uint32_t>(C, std::max<uint32_t>(kMaxSteps, 16 * rc));
-        std::vector<Item> chunks, whole;
+        std::vector<Item> all;
         std::vector<CombineTree> ctrees;
+        s.slice_items.assign(G + 1, 0);
         uint32_t nch = 0;
-        for (uint32_t t = 0; t < ts.count; ++t) {
-            const uint32_t n = ts.h_size[t];
-            if (n <= C) {
-                whole.push_back({t, kWholeTree, 0, n});
-                continue;
+        for (uint32_t g = 0; g < G; ++g) {
+            s.slice_items[g] = (uint32_t)all.size();
+            std::vector<Item> whole;
+            for (uint32_t t = tb[g]; t < tb[g + 1]; ++t) {
+                const uint32_t n = ts.h_size[t];
+                if (n <= C) {
+                    whole.push_back({t, kWholeTree, 0, n});
+                    continue;
+                }
+                const uint32_t k = (n + C - 1) / C;
+                ctrees.push_back({t, nch, k, n});
+                for (uint32_t j = 0; j < k; ++j) all.push_back({t, nch + j, j * C, std::min(n, (j + 1) * C)});
+                nch += k;
             }
-            const uint32_t k = (n + C - 1) / C;
-            ctrees.push_back({t, nch, k, n});
-            for (uint32_t j = 0; j < k; ++j) chunks.push_back({t, nch + j, j * C, std::min(n, (j + 1) * C)});
-            nch += k;
+            std::stable_sort(whole.begin(), whole.end(),
+                             [](const Item& x, const Item& y) { return x.hi > y.hi; });
+            all.insert(all.end(), whole.begin(), whole.end());
         }
-        std::stable_sort(whole.begin(), whole.end(),
-                         [](const Item& a, const Item& b) { return a.hi > b.hi; });
-        const uint32_t nitems = (uint32_t)(chunks.size() + whole.size());
+        s.slice_items[G] = (uint32_t)all.size();
+        const uint32_t nitems = (uint32_t)all.size();
         // the pinned staging buffers are reused: wait for older copies
         CK(cudaStreamSynchronize(s.st));
         TRY(s.h_items.ensure(sizeof(Item) * std::max<uint32_t>(nitems, 1)));
-        Item* hi = s.h_items.as<Item>();
-        std::copy(chunks.begin(), chunks.end(), hi);
-        std::copy(whole.begin(), whole.end(), hi + chunks.size());
+        std::copy(all.begin(), all.end(), s.h_items.as<Item>());
         TRY(s.items.ensure(sizeof(Item) * std::max<uint32_t>(nitems, 1), s.dev));
-        if (nitems) CK(cudaMemcpyAsync(s.items.p, hi, sizeof(Item) * nitems, cudaMemcpyHostToDevice, s.st));
+        if (nitems) CK(cudaMemcpyAsync(s.items.p, s.h_items.p, sizeof(Item) * nitems, cudaMemcpyHostToDevice, s.st));
         const uint32_t nct = (uint32_t)ctrees.size();
         if (nct) {
             TRY(s.h_ctrees.ensure(sizeof(CombineTree) * nct));
@@ -319,12 +364,12 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         s.last_ctrees = nct;
         s.items_for = &ts;
         s.items_version = ts.version;
+        s.items_slices = tb;
     }
-    const uint32_t nitems = s.last_items, nch = s.last_chunks, nct = s.last_ctrees;
-    (void)nch;
+    const uint32_t nitems = s.last_items, nct = s.last_ctrees;
     TRY(s.rec.ensure(sizeof(ltgp_record) * std::max<uint32_t>(ts.count, 1), s.dev));
     if (want_outs) TRY(s.outs.ensure(sizeof(float) * kLanes * std::max<uint32_t>(ts.count, 1), s.dev));
-    CK(cudaMemsetAsync(s.counters.p, 0, 64, s.st));
+    CK(cudaMemsetAsync(s.counters.p, 0, kCounterBytes, s.st));
     EvalArgs& a = s.eargs;
     a.arena = ts.arena.as<uint8_t>();
     a.off = ts.off.as<uint64_t>();
@@ -332,6 +377,8 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     a.items = s.items.as<Item>();
     a.n_items = nitems;
     a.counters = s.counters.as<uint32_t>();
+    a.queue = s.counters.as<uint32_t>();
+    a.item_base = 0;
     a.hdr = s.hdr.as<ChunkHdr>();
     a.steps = s.steps.as<uint8_t>();
     a.frames = s.frames.as<float2>();
@@ -362,28 +409,59 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     uint4* dec = ts.decode.as<uint4>();
     a.decode = dec;
     a.packets = packets;
+    if (streamed) TRY(s.spill2.ensure(s.spill.bytes, s.dev));
     CK(cudaEventRecord(s.ev[0], s.st));
     uint32_t launches = 0;
-    if (packets) {
-        const uint64_t blocks = std::min<uint64_t>((packets + 255) / 256, (uint64_t)s.sms * 16);
-        k_decode<<<(unsigned)blocks, 256, 0, s.st>>>(ts.arena.as<uint4>(), dec, packets);
-        CK(cudaGetLastError());
-        DEBUG_SYNC(s.st, "k_decode");
-        ++launches;
+    for (uint32_t g = 0; g < G; ++g) {
+        cudaStream_t X = (g & 1u) ? s.st2 : s.st;
+        uint64_t p_lo = 0, p_hi = packets;
+        if (streamed) {
+            const Slice& sl = s.slices[g];
+            if (g == 0) CK(cudaStreamWaitEvent(s.cst, s.ev[0], 0));  // counters cleared, arena free
+            CK(cudaMemcpyAsync(ts.arena.as<uint8_t>() + sl.dst, s.src + sl.src, sl.len, cudaMemcpyHostToDevice,
+                               s.cst));
+            CK(cudaEventRecord(s.sev[3 * g], s.cst));
+            CK(cudaStreamWaitEvent(X, s.sev[3 * g], 0));
+            // the previous slice's records are final before this slice's
+            // kernels (its k_eval's look-ahead may read them)
+            if (g > 0) CK(cudaStreamWaitEvent(X, s.sev[3 * (g - 1) + 1], 0));
+            p_lo = sl.dst / 16;
+            p_hi = (sl.dst + sl.len + 15) / 16;
+        }
+        const uint32_t i0 = s.slice_items[g], ni = s.slice_items[g + 1] - i0;
+        if (p_hi > p_lo) {
+            const uint64_t blocks = std::min<uint64_t>((p_hi - p_lo + 255) / 256, (uint64_t)s.sms * 16);
+            k_decode<<<(unsigned)blocks, 256, 0, X>>>(ts.arena.as<uint4>(), dec, packets, p_lo, p_hi);
+            CK(cudaGetLastError());
+            DEBUG_SYNC(X, "k_decode");
+            ++launches;
+        }
+        if (ni) {
+            k_plan<<<(ni + 127) / 128, 128, 0, X>>>(s.items.as<Item>() + i0, ni, ts.off.as<uint64_t>(),
+                                                   reinterpret_cast<uint8_t*>(dec), packets, kWindow);
+            CK(cudaGetLastError());
+            DEBUG_SYNC(X, "k_plan");
+            ++launches;
+        }
+        if (streamed) CK(cudaEventRecord(s.sev[3 * g + 1], X));
+        if (ni) {
+            EvalArgs ag = a;
+            ag.items = a.items + i0;
+            ag.n_items = ni;
+            ag.item_base = i0;
+            ag.queue = s.counters.as<uint32_t>() + kQueueBase + g;
+            if (g & 1u) ag.spill = s.spill2.as<float2>();
+            const int grid = std::min<int>(s.eval_grid, (int)ni);
+            K_EVAL<<<std::max(grid, 1), kWarps * 32, eval_smem_bytes(), X>>>(ag, e->suite);
+            CK(cudaGetLastError());
+            DEBUG_SYNC(X, "k_eval");
+            ++launches;
+        }
+        if (streamed) CK(cudaEventRecord(s.sev[3 * g + 2], X));
     }
-    if (nitems) {
-        k_plan<<<(nitems + 127) / 128, 128, 0, s.st>>>(s.items.as<Item>(), nitems, ts.off.as<uint64_t>(),
-                                                      reinterpret_cast<uint8_t*>(dec), packets, kWindow);
-        CK(cudaGetLastError());
-        DEBUG_SYNC(s.st, "k_plan");
-        ++launches;
-    }
-    if (nitems) {
-        const int grid = std::min<int>(s.eval_grid, (int)nitems);
-        K_EVAL<<<std::max(grid, 1), kWarps * 32, eval_smem_bytes(), s.st>>>(a, e->suite);
-        CK(cudaGetLastError());
-        DEBUG_SYNC(s.st, "k_eval");
-        ++launches;
+    if (streamed && G > 1) {  // join the second compute stream (odd slices)
+        const uint32_t last_odd = ((G - 1) & 1u) ? G - 1 : G - 2;
+        CK(cudaStreamWaitEvent(s.st, s.sev[3 * last_odd + 2], 0));
     }
     CK(cudaEventRecord(s.ev[4], s.st));
     if (nct) {
@@ -683,8 +761,11 @@ int ltgp_set_suite(ltgp_engine* e, const float* in, const float* tg, const float
     return 0;
 }
 
-int ltgp_upload_packed(ltgp_engine* e, uint32_t M, const uint8_t* buf, uint64_t buf_bytes,
-                       const uint64_t* offsets, const uint64_t* sizes) {
+}  // extern "C"
+
+namespace {
+int check_packed(const ltgp_engine* e, uint32_t M, const uint8_t* buf, uint64_t buf_bytes, const uint64_t* offsets,
+                 const uint64_t* sizes) {
     if (!e || (M && (!buf || !offsets || !sizes))) { set_err("null argument"); return -1; }
     for (uint32_t i = 0; i < M; ++i) {
         if (offsets[i] % 16) { set_err("offset of genome %u not 16-aligned", i); return -1; }
@@ -694,6 +775,15 @@ int ltgp_upload_packed(ltgp_engine* e, uint32_t M, const uint8_t* buf, uint64_t 
             return -1;
         }
     }
+    return 0;
+}
+}  // namespace
+
+extern "C" {
+
+int ltgp_upload_packed(ltgp_engine* e, uint32_t M, const uint8_t* buf, uint64_t buf_bytes,
+                       const uint64_t* offsets, const uint64_t* sizes) {
+    TRY(check_packed(e, M, buf, buf_bytes, offsets, sizes));
     partition(e, M, sizes);
     for (Shard& s : e->shards) {
         s.cur = 0;
@@ -759,6 +849,49 @@ int ltgp_evaluate_collect(ltgp_engine* e, ltgp_record* out, uint64_t* nodes) {
 int ltgp_evaluate_population(ltgp_engine* e, ltgp_record* out, uint64_t* nodes) {
     TRY(ltgp_evaluate_launch(e));
     return ltgp_evaluate_collect(e, out, nodes);
+}
+
+int ltgp_evaluate_packed(ltgp_engine* e, uint32_t M, const uint8_t* buf, uint64_t buf_bytes,
+                         const uint64_t* offsets, const uint64_t* sizes, ltgp_record* out, float* outs48) {
+    TRY(check_packed(e, M, buf, buf_bytes, offsets, sizes));
+    if (!e->have_suite) { set_err("ltgp_set_suite not called"); return -1; }
+    partition(e, M, sizes);
+    for (Shard& s : e->shards) {
+        s.cur = 0;
+        TreeSet& ts = s.set[0];
+        if (s.count == 0) { ts.count = 0; continue; }
+        TRY(set_layout(s, ts, s.count, sizes + s.first, nullptr));
+        // slices of ~kSliceBytes at tree boundaries, laid out kSlicePad apart
+        const uint64_t base = offsets[s.first];
+        const uint64_t last = s.first + s.count - 1;
+        const uint64_t end = std::min<uint64_t>(ceil16(offsets[last] + sizes[last]), buf_bytes);
+        const uint64_t span = end - base;
+        const uint32_t G = (uint32_t)std::min<uint64_t>(kMaxSlices, std::max<uint64_t>(1, span / kSliceBytes));
+        s.slices.clear();
+        uint32_t t = 0;
+        uint64_t dst = 0;
+        for (uint32_t g = 0; g < G && t < s.count; ++g) {
+            const uint64_t goal = base + span * (g + 1) / G;
+            const uint32_t t0 = t;
+            do { ++t; } while (t < s.count && (g == G - 1 || offsets[s.first + t] < goal));
+            const uint64_t src = offsets[s.first + t0];
+            const uint64_t stop = t < s.count ? offsets[s.first + t] : end;
+            s.slices.push_back({t0, src, dst, stop - src});
+            for (uint32_t i = t0; i < t; ++i) ts.h_off[i] = dst + (offsets[s.first + i] - src);
+            dst = ceil16(dst + (stop - src)) + kSlicePad;
+        }
+        const Slice& ls = s.slices.back();
+        ts.bytes = ls.dst + ls.len;
+        TRY(ts.arena.ensure(ts.bytes + 64, s.dev));
+        TRY(upload_tables(s, ts));
+        s.src = buf;
+        const int rc = launch_eval(e, s, ts, outs48 != nullptr);
+        s.slices.clear();
+        s.src = nullptr;
+        TRY(rc);
+    }
+    e->M = M;
+    return collect(e, out, outs48);
 }
 
 int ltgp_evaluate_outputs(ltgp_engine* e, ltgp_record* out, float* outs48) {

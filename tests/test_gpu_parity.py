@@ -246,6 +246,43 @@ def test_config3_full_size_sampled(oracle, suite):
     assert_records_equal(rec, exp)
 
 
+def test_streamed_evaluate_packed_matches_resident(oracle, suite):
+    """ltgp_evaluate_packed (upload in ~32 MB slices overlapped with their
+    evaluation; the full config-3 corpus is 16 slices) gives the same records
+    as the resident path, on one shard and on two; and again on reuse (cached
+    work list, arena reused while the previous call's data is still there)."""
+    buf, offs, sizes = ltgp.corpus(1, 4000, 4.0, 6.0)
+    with engine(suite) as e:
+        e.upload_packed(buf, offs, sizes)
+        exp = e.evaluate_population()
+        got = e.evaluate_packed(buf, offs, sizes)
+        assert got.tobytes() == exp.tobytes()
+        got2 = e.evaluate_packed(buf, offs, sizes)
+        assert got2.tobytes() == exp.tobytes()
+        assert e.evaluate_population().tobytes() == exp.tobytes()  # population = the streamed one
+    with engine(suite, devices=(0, 0)) as e:
+        assert e.evaluate_packed(buf, offs, sizes).tobytes() == exp.tobytes()
+    # and against the oracle on a sample of slots
+    idx = np.arange(0, 4000, 97)
+    sub = [buf[int(offs[k]):int(offs[k]) + int(sizes[k])].copy() for k in idx]
+    b2, o2, s2 = pack(sub)
+    ref = oracle.evaluate_population(b2, o2, s2, suite, threads=0)
+    assert_records_equal(got[idx], ref)
+
+
+def test_streamed_small_and_outputs(oracle, suite):
+    """A small population (one slice) with per-case outputs, from pageable memory."""
+    genomes = [ltgp.remy_tree(70 + k, n) for k, n in enumerate((1, 3, 17, 1001, 20001, 70001))]
+    buf, offs, sizes = pack(genomes)
+    with engine(suite, chunk=1024) as e:
+        rec, outs = e.evaluate_packed(buf, offs, sizes, outputs=True)
+    exp = oracle.evaluate_population(buf, offs, sizes, suite, threads=0)
+    assert_records_equal(rec, exp)
+    for k, g in enumerate(genomes):
+        o, _ = oracle.eval_batch(g, suite[0], suite[2])
+        assert same_bits(outs[k], o)
+
+
 @pytest.mark.slow
 def test_config2_bloating_run_matches_oracle(oracle, tmp_path):
     """Config 2 scale: pop 4000, tournament 7, no size limit, 100 generations
