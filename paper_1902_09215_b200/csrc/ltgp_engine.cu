@@ -162,22 +162,33 @@ struct Slice {
     uint32_t tree_begin;
     uint64_t src, dst, len;
 };
-constexpr uint32_t kMaxSlices = 16;
+constexpr uint32_t kMaxSlices = 64;
+constexpr int kComputeStreams = 4;     // slice g runs on compute stream g % 4
 constexpr uint64_t kSlicePad = 2048;   // arena gap between slices (k_eval's record look-ahead < 1 KB)
-constexpr uint64_t kSliceBytes = 32ull << 20;  // target bytes per slice
+// target bytes per slice, slice count cap (LTGP_SLICE_MB / LTGP_SLICES override)
+uint64_t slice_bytes() {
+    static const uint64_t v = std::getenv("LTGP_SLICE_MB") ? std::atoll(std::getenv("LTGP_SLICE_MB")) << 20 : 32ull << 20;
+    return v;
+}
+uint32_t max_slices() {
+    static const uint32_t v = std::getenv("LTGP_SLICES") ? std::min<uint32_t>(kMaxSlices, std::atoi(std::getenv("LTGP_SLICES")))
+                                                         : 16u;
+    return v;
+}
 constexpr uint32_t kQueueBase = 16;    // counters[16 + g]: work queue of slice g
 constexpr size_t kCounterBytes = 256;
 
 struct Shard {
     int dev = 0;
     cudaStream_t st = nullptr;
-    cudaStream_t st2 = nullptr, cst = nullptr;  // second compute stream, copy stream (streamed evaluation)
+    cudaStream_t xs[kComputeStreams] = {};      // compute streams of a streamed evaluation (xs[0] = st)
+    cudaStream_t cst = nullptr;                 // its copy stream
     std::vector<cudaEvent_t> sev;               // 3 per slice: copied, planned, evaluated
     std::vector<Slice> slices;                  // non-empty during a streamed evaluation
     const uint8_t* src = nullptr;               // its pinned host source
     std::vector<uint32_t> slice_items;          // slice g's items: [slice_items[g], slice_items[g+1])
     std::vector<uint32_t> items_slices;         // work-list cache key (slice tree boundaries)
-    DevBuf spill2;                              // spill area of the second compute stream
+    DevBuf xspill[kComputeStreams];             // spill areas of xs[1..] (xs[0] uses spill)
     cudaEvent_t ev[8] = {};
     int sms = 0;
     int eval_grid = 0;
@@ -209,9 +220,9 @@ struct Shard {
                           &rerun_slot[1], &ovf, &big_spill}) b->release();
         h_items.release(); h_ctrees.release(); h_counters.release();
         h_csize.release(); h_coff.release(); h_dir.release();
-        spill2.release();
+        for (auto& b : xspill) b.release();
         if (st) { cudaSetDevice(dev); cudaStreamDestroy(st); }
-        if (st2) cudaStreamDestroy(st2);
+        for (int k = 1; k < kComputeStreams; ++k) if (xs[k]) cudaStreamDestroy(xs[k]);
         if (cst) cudaStreamDestroy(cst);
         for (auto& e : ev) if (e) cudaEventDestroy(e);
         for (auto& e : sev) if (e) cudaEventDestroy(e);
@@ -246,7 +257,8 @@ uint32_t spill_frames() {  // LTGP_SPILL_FRAMES overrides (debugging)
 int init_shard(ltgp_engine* e, Shard& s) {
     CK(cudaSetDevice(s.dev));
     CK(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&s.st2, cudaStreamNonBlocking));
+    s.xs[0] = s.st;
+    for (int k = 1; k < kComputeStreams; ++k) CK(cudaStreamCreateWithFlags(&s.xs[k], cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&s.cst, cudaStreamNonBlocking));
     for (auto& ev : s.ev) CK(cudaEventCreate(&ev));
     s.sev.resize(3 * kMaxSlices);
@@ -277,9 +289,10 @@ int init_shard(ltgp_engine* e, Shard& s) {
 // Streamed evaluation (s.slices non-empty, ltgp_evaluate_packed): the trees
 // arrive from pinned host memory in slices (consecutive trees, each slice
 // 2 KB apart in the arena). Slice g's bytes go over a copy stream; its
-// k_decode, k_plan and k_eval start as soon as they land, alternating between
-// two compute streams so one slice's k_eval fills the SMs the previous
-// slice's tail frees. The upload overlaps the evaluation. Without slices the
+// k_decode, k_plan and k_eval start as soon as they land, on compute stream
+// g % 4: a slice's k_eval lasts at least one work item's latency, so slices
+// must not queue behind each other, and each k_eval fills the SMs the earlier
+// slices' tails free. The upload overlaps the evaluation. Without slices the
 // arena is resident and the whole set is one slice on s.st.
 int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     CK(cudaSetDevice(s.dev));
@@ -409,11 +422,13 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     uint4* dec = ts.decode.as<uint4>();
     a.decode = dec;
     a.packets = packets;
-    if (streamed) TRY(s.spill2.ensure(s.spill.bytes, s.dev));
+    if (streamed)
+        for (int k = 1; k < kComputeStreams && k < (int)G; ++k) TRY(s.xspill[k].ensure(s.spill.bytes, s.dev));
     CK(cudaEventRecord(s.ev[0], s.st));
     uint32_t launches = 0;
     for (uint32_t g = 0; g < G; ++g) {
-        cudaStream_t X = (g & 1u) ? s.st2 : s.st;
+        const uint32_t xk = g % kComputeStreams;
+        cudaStream_t X = s.xs[xk];
         uint64_t p_lo = 0, p_hi = packets;
         if (streamed) {
             const Slice& sl = s.slices[g];
@@ -450,7 +465,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             ag.n_items = ni;
             ag.item_base = i0;
             ag.queue = s.counters.as<uint32_t>() + kQueueBase + g;
-            if (g & 1u) ag.spill = s.spill2.as<float2>();
+            if (xk) ag.spill = s.xspill[xk].as<float2>();
             const int grid = std::min<int>(s.eval_grid, (int)ni);
             K_EVAL<<<std::max(grid, 1), kWarps * 32, eval_smem_bytes(), X>>>(ag, e->suite);
             CK(cudaGetLastError());
@@ -459,10 +474,9 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         }
         if (streamed) CK(cudaEventRecord(s.sev[3 * g + 2], X));
     }
-    if (streamed && G > 1) {  // join the second compute stream (odd slices)
-        const uint32_t last_odd = ((G - 1) & 1u) ? G - 1 : G - 2;
-        CK(cudaStreamWaitEvent(s.st, s.sev[3 * last_odd + 2], 0));
-    }
+    if (streamed)  // join the other compute streams: the last slice each ran
+        for (uint32_t g = G > (uint32_t)kComputeStreams ? G - kComputeStreams : 0; g < G; ++g)
+            if (g % kComputeStreams) CK(cudaStreamWaitEvent(s.st, s.sev[3 * g + 2], 0));
     CK(cudaEventRecord(s.ev[4], s.st));
     if (nct) {
         const int blocks = (int)std::min<uint32_t>((nct + kCombineWarps - 1) / kCombineWarps, (uint32_t)s.sms * 16);
@@ -866,7 +880,7 @@ int ltgp_evaluate_packed(ltgp_engine* e, uint32_t M, const uint8_t* buf, uint64_
         const uint64_t last = s.first + s.count - 1;
         const uint64_t end = std::min<uint64_t>(ceil16(offsets[last] + sizes[last]), buf_bytes);
         const uint64_t span = end - base;
-        const uint32_t G = (uint32_t)std::min<uint64_t>(kMaxSlices, std::max<uint64_t>(1, span / kSliceBytes));
+        const uint32_t G = (uint32_t)std::min<uint64_t>(max_slices(), std::max<uint64_t>(1, span / slice_bytes()));
         s.slices.clear();
         uint32_t t = 0;
         uint64_t dst = 0;
