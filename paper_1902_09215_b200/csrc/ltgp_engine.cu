@@ -28,8 +28,8 @@ using namespace ltgp_dev;
 
 namespace {
 
-constexpr int kWarps = 28;           // warps per k_eval CTA (one CTA per SM)
-constexpr int kWindow = 25;          // shared stack window frames per warp
+constexpr int kWarps = 32;           // warps per k_eval CTA (one CTA per SM)
+constexpr int kWindow = 20;          // shared stack window frames per warp
 constexpr uint32_t kDefaultChunk = 16384;
 constexpr uint32_t kMaxSteps = 1024;
 constexpr uint32_t kMaxFrames = 256;
