@@ -35,6 +35,7 @@ constexpr uint32_t kMaxSteps = 1024;
 constexpr uint32_t kMaxFrames = 256;
 constexpr uint32_t kMaxChunk = 65536;      // automatic chunk length ceiling
 constexpr uint64_t kCombineChunks = 128;   // target chunks per tree (sequential combine)
+constexpr uint32_t kPlanWarpChunk = 32768; // chunk length from which k_plan_warp plans (a warp per item)
 constexpr uint32_t kSpillFrames = 1024;  // per warp; items that need more are re-run
 constexpr int kRerunCtas = 8;
 
@@ -145,13 +146,13 @@ inline uint64_t ceil16(uint64_t x) { return (x + 15) & ~uint64_t(15); }
 
 // A set of trees resident on one device: tree i at arena + off[i].
 struct TreeSet {
-    DevBuf arena, off, size, decode;
+    DevBuf arena, off, size, decode, meta;
     std::vector<uint64_t> h_off;
     std::vector<uint32_t> h_size;
     uint32_t count = 0;
     uint64_t bytes = 0;   // used arena bytes
     uint64_t version = 0; // bumped whenever the layout (sizes) changes
-    void release() { arena.release(); off.release(); size.release(); decode.release(); }
+    void release() { arena.release(); off.release(); size.release(); decode.release(); meta.release(); }
 };
 
 uint64_t g_version = 0;
@@ -176,6 +177,7 @@ uint32_t max_slices() {
     return v;
 }
 constexpr uint32_t kQueueBase = 16;    // counters[16 + g]: work queue of slice g
+constexpr uint32_t kPoolCounters = 8;  // counters[8..11]: chunk-summary pool claims (2 x u64)
 constexpr size_t kCounterBytes = 256;
 
 struct Shard {
@@ -205,6 +207,7 @@ struct Shard {
     HostBuf h_items, h_ctrees, h_counters;
     uint32_t last_items = 0, last_chunks = 0, last_ctrees = 0;
     uint32_t cur_chunk = kDefaultChunk, cur_max_frames = kMaxFrames, cur_max_steps = kMaxSteps;
+    double pool_per_chunk_f = 0.0, pool_per_chunk_s = 0.0;  // summary pool claimed per chunk (last evaluation)
     EvalArgs eargs;      // arguments of the last evaluation (for overflow reruns)
     CombineArgs cargs;
     const TreeSet* items_for = nullptr;  // work list cache: (set, version)
@@ -322,9 +325,10 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             while (C < kDefaultChunk && (uint64_t)C * 2 <= per) C *= 2;
             while (C < kMaxChunk && (uint64_t)C * kCombineChunks < biggest) C *= 2;
         }
-        // summary capacities: a chunk's spine and its frames (K frames +
-        // outputs) grow like sqrt(C) (Remy-random trees: mean ~1.6 sqrt(C),
-        // max ~3.6 sqrt(C) frames, ~6 sqrt(C) steps)
+        // chunk summaries are sized exactly by k_plan (PlanPool); these are
+        // the per-chunk capacities of the first overflow re-run tier (x4).
+        // A chunk's spine and frames grow like sqrt(C) (Remy-random trees:
+        // mean ~1.6 sqrt(C), max ~3.6 sqrt(C) frames, ~6 sqrt(C) steps)
         const uint32_t rc = (uint32_t)std::lround(std::sqrt((double)C));
         s.cur_chunk = C;
         s.cur_max_frames = std::max<uint32_t>(kMaxFrames, (6 * rc + 63) & ~63u);
@@ -367,8 +371,6 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             CK(cudaMemcpyAsync(s.ctrees.p, s.h_ctrees.p, sizeof(CombineTree) * nct,
                                cudaMemcpyHostToDevice, s.st));
             TRY(s.hdr.ensure(sizeof(ChunkHdr) * nch, s.dev));
-            TRY(s.steps.ensure((size_t)s.cur_max_steps * nch, s.dev));
-            TRY(s.frames.ensure((size_t)s.cur_max_frames * kFrameBytes * nch, s.dev));
             TRY(s.dframes.ensure((size_t)kFrameBytes * nch, s.dev));
             TRY(s.segs.ensure(sizeof(Seg) * 2 * nch, s.dev));
         }
@@ -379,7 +381,24 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         s.items_version = ts.version;
         s.items_slices = tb;
     }
-    const uint32_t nitems = s.last_items, nct = s.last_ctrees;
+    const uint32_t nitems = s.last_items, nct = s.last_ctrees, nch = s.last_chunks;
+    // chunk-summary pool (k_plan claims every chunk's exact summary): an
+    // estimate per chunk (Remy-random chunks: mean 1.6 sqrt(C) frames and
+    // steps), raised to what earlier evaluations actually claimed per chunk
+    PlanPool pool{};
+    if (nch) {
+        const double rc = std::sqrt((double)s.cur_chunk);
+        const double pf = std::max(std::min(2.0 * rc, (double)s.cur_chunk + 2), s.pool_per_chunk_f * 1.25);
+        const double ps = std::max(std::min(2.0 * rc, (double)s.cur_chunk), s.pool_per_chunk_s * 1.25);
+        pool.cap_frames = (unsigned long long)(pf * nch) + 64;
+        pool.cap_steps = (unsigned long long)(ps * nch) + 1024;
+        TRY(s.frames.ensure((size_t)pool.cap_frames * kFrameBytes, s.dev));
+        TRY(s.steps.ensure((size_t)pool.cap_steps, s.dev));
+        pool.hdr = s.hdr.as<ChunkHdr>();
+        pool.frames = s.frames.as<float2>();
+        pool.steps = s.steps.as<uint8_t>();
+        pool.used = reinterpret_cast<unsigned long long*>(s.counters.as<uint32_t>() + kPoolCounters);
+    }
     TRY(s.rec.ensure(sizeof(ltgp_record) * std::max<uint32_t>(ts.count, 1), s.dev));
     if (want_outs) TRY(s.outs.ensure(sizeof(float) * kLanes * std::max<uint32_t>(ts.count, 1), s.dev));
     CK(cudaMemsetAsync(s.counters.p, 0, kCounterBytes, s.st));
@@ -395,8 +414,8 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     a.hdr = s.hdr.as<ChunkHdr>();
     a.steps = s.steps.as<uint8_t>();
     a.frames = s.frames.as<float2>();
-    a.max_steps = s.cur_max_steps;
-    a.max_frames = s.cur_max_frames;
+    a.max_steps = 0xffffffffu;   // first pass: k_plan's exact buffers (checked at item end)
+    a.max_frames = 0xffffffffu;
     a.spill = s.spill.as<float2>();
     a.spill_frames = spill_frames();
     TRY(s.ovf.ensure(sizeof(uint32_t) * std::max<uint32_t>(nitems, 1), s.dev));
@@ -419,6 +438,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     const uint64_t packets = (ts.bytes + 15) / 16;
     // +1 KB: the fast path stages record groups up to 512 B past an item
     TRY(ts.decode.ensure(std::max<uint64_t>(packets, 1) * 32 + 1024, s.dev));
+    TRY(ts.meta.ensure(std::max<uint64_t>(packets, 1) * 4, s.dev));
     uint4* dec = ts.decode.as<uint4>();
     a.decode = dec;
     a.packets = packets;
@@ -446,14 +466,23 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         const uint32_t i0 = s.slice_items[g], ni = s.slice_items[g + 1] - i0;
         if (p_hi > p_lo) {
             const uint64_t blocks = std::min<uint64_t>((p_hi - p_lo + 255) / 256, (uint64_t)s.sms * 16);
-            k_decode<<<(unsigned)blocks, 256, 0, X>>>(ts.arena.as<uint4>(), dec, packets, p_lo, p_hi);
+            k_decode<<<(unsigned)blocks, 256, 0, X>>>(ts.arena.as<uint4>(), dec, ts.meta.as<uint32_t>(), packets,
+                                                     p_lo, p_hi);
             CK(cudaGetLastError());
             DEBUG_SYNC(X, "k_decode");
             ++launches;
         }
-        if (ni) {
+        if (ni && s.cur_chunk >= kPlanWarpChunk) {  // long items: a warp per item
+            k_plan_warp<<<(ni + 3) / 4, 128, 0, X>>>(s.items.as<Item>() + i0, ni, ts.off.as<uint64_t>(),
+                                                    reinterpret_cast<uint8_t*>(dec), ts.meta.as<uint32_t>(),
+                                                    packets, kWindow, pool);
+            CK(cudaGetLastError());
+            DEBUG_SYNC(X, "k_plan_warp");
+            ++launches;
+        } else if (ni) {
             k_plan<<<(ni + 127) / 128, 128, 0, X>>>(s.items.as<Item>() + i0, ni, ts.off.as<uint64_t>(),
-                                                   reinterpret_cast<uint8_t*>(dec), packets, kWindow);
+                                                   reinterpret_cast<uint8_t*>(dec), ts.meta.as<uint32_t>(), packets,
+                                                   kWindow, pool);
             CK(cudaGetLastError());
             DEBUG_SYNC(X, "k_plan");
             ++launches;
@@ -594,6 +623,7 @@ int check_eval(Shard& s) {
         return -1;
     }
     if (flags & 8u) { set_err("k_eval shared-memory layout does not fit"); return -1; }
+    if (flags & 16u) { set_err("chunk summary differs from k_plan's sizing (internal error)"); return -1; }
     if (flags & 2u) { set_err("malformed genome (stack underflow or leftover values)"); return -1; }
     return 0;
 }
@@ -601,6 +631,13 @@ int check_eval(Shard& s) {
 // After the stream is synchronized: re-run overflowed chunks if any.
 int finish_eval(ltgp_engine* e, Shard& s) {
     const uint32_t* c = s.h_counters.as<uint32_t>();
+    if (s.last_chunks) {  // what this evaluation's chunks claimed from the summary pool
+        uint64_t uf, us;
+        std::memcpy(&uf, c + kPoolCounters, 8);
+        std::memcpy(&us, c + kPoolCounters + 2, 8);
+        s.pool_per_chunk_f = (double)uf / s.last_chunks;
+        s.pool_per_chunk_s = (double)us / s.last_chunks;
+    }
     if (c[2] != 0) TRY(rerun_overflowed(e, s));
     return check_eval(s);
 }

@@ -135,17 +135,25 @@ def test_adversarial(oracle, suite):
 
 
 def test_capacity_overflow_reruns(oracle, suite):
-    """Items whose stack outgrows the per-warp spill area (a 16001-node left
-    chain is one whole-tree item holding 8001 values; its 64-node chunks are
-    all leaves) are re-run with worst-case capacities, bit-exactly."""
+    """Work items that outgrow a capacity are re-run with worst-case capacities,
+    bit-exactly: whole-tree items whose stack outgrows the per-warp spill area
+    (chunk 65536: a 16001-node left chain holds 8001 values), and chunks of
+    4096 leaves (their stack outgrows the spill area and their summaries the
+    sqrt(C)-sized summary pool). All-leaf 64-node chunks overflow only the
+    pool's first estimate: the second evaluation sizes the pool from the
+    first one's exact claims and needs no re-run."""
     gs = [np.array([ADD] * 8000 + [X] + [5 + 7] * 8000, np.uint8),
           np.array([SUB] * 5000 + [X] + [5 + (k % 250) for k in range(5000)], np.uint8)]
-    for chunk, reruns in ((0, None), (64, 0), (4096, 7)):
+    for chunk, rerun in ((64, False), (4096, True), (65536, True)):
         with engine(suite, chunk=chunk) as e:
             e.upload_population(gs)
             rec, outs = e.evaluate_outputs()
             n = e.stats()["last_fallback_items"]
-            assert n == reruns if reruns is not None else n > 0
+            assert n > 0 or not rerun, (chunk, n)
+            rec2, outs2 = e.evaluate_outputs()
+            n2 = e.stats()["last_fallback_items"]
+            assert (n2 > 0) == rerun, (chunk, n2)
+            assert rec2.tobytes() == rec.tobytes() and same_bits(outs2, outs)
         for k, g in enumerate(gs):
             o, _ = oracle.eval_batch(g, suite[0], suite[2])
             assert same_bits(outs[k], o)
