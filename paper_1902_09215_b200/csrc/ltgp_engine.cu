@@ -33,8 +33,7 @@ constexpr int kWindow = 20;          // shared stack window frames per warp
 constexpr uint32_t kDefaultChunk = 16384;
 constexpr uint32_t kMaxSteps = 1024;
 constexpr uint32_t kMaxFrames = 256;
-constexpr uint32_t kMaxChunk = 65536;      // automatic chunk length ceiling
-constexpr uint64_t kCombineChunks = 128;   // target chunks per tree (sequential combine)
+constexpr uint32_t kMaxChunk = 524288;     // automatic chunk length ceiling
 constexpr uint32_t kPlanWarpChunk = 32768; // chunk length from which k_plan_warp plans (a warp per item)
 constexpr uint32_t kSpillFrames = 1024;  // per warp; items that need more are re-run
 constexpr int kRerunCtas = 8;
@@ -250,10 +249,19 @@ namespace {
 
 static_assert(EvalLayout<kWarps, kWindow>::kBytes <= 227u * 1024u, "k_eval needs more than 227 KB of shared memory");
 size_t eval_smem_bytes() { return EvalLayout<kWarps, kWindow>::kBytes; }
-uint32_t spill_frames() {  // LTGP_SPILL_FRAMES overrides (debugging)
+uint32_t spill_frames_base() {  // LTGP_SPILL_FRAMES overrides (debugging)
     static const uint32_t v = std::getenv("LTGP_SPILL_FRAMES") ? (uint32_t)std::atoi(std::getenv("LTGP_SPILL_FRAMES"))
                                                                 : kSpillFrames;
     return v;
+}
+// per-warp spill frames for chunk length C: a chunk's stack (a random walk
+// for random trees) reaches a few sqrt(C) frames; deeper items are re-run
+uint32_t spill_frames(uint32_t C) {
+    if (std::getenv("LTGP_SPILL_FRAMES")) return spill_frames_base();
+    uint32_t f = spill_frames_base();
+    const uint32_t want = (uint32_t)(8.0 * std::sqrt((double)C));
+    while (f < want) f *= 2;
+    return f;
 }
 #define K_EVAL k_eval<kWarps, kWindow>
 
@@ -280,7 +288,7 @@ int init_shard(ltgp_engine* e, Shard& s) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K_EVAL, kWarps * 32, smem));
     if (per_sm < 1) { set_err("k_eval does not fit on an SM"); return -1; }
     s.eval_grid = per_sm * s.sms;
-    TRY(s.spill.ensure((size_t)s.eval_grid * kWarps * spill_frames() * kFrameBytes, s.dev));
+    TRY(s.spill.ensure((size_t)s.eval_grid * kWarps * spill_frames_base() * kFrameBytes, s.dev));
     TRY(s.counters.ensure(kCounterBytes, s.dev));
     TRY(s.h_counters.ensure(64));
     return 0;
@@ -310,9 +318,10 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         // chunk length: the configured one, or sized so the persistent grid
         // gets >= ~2 items per warp (small populations must not wait on one
         // warp per tree; more chunks cost combine work), 1024..16384 nodes;
-        // and long enough that the largest tree has at most kCombineChunks
-        // chunks, up to kMaxChunk, since k_combine replays one tree's chunks
-        // sequentially (a lone huge tree)
+        // and, for huge trees, long enough to balance one item's scan latency
+        // (~C / 13e6 s) against the largest tree's sequential combine (~N/C
+        // chunks x 1.6 sqrt(C) spine steps x ~60 ns): C ~ (1.25 N)^(2/3),
+        // up to kMaxChunk (1e7 nodes: 65536; 4e8 nodes: 524288)
         uint32_t C = e->chunk;
         if (!e->chunk_fixed) {
             uint64_t total = 0, biggest = 0;
@@ -323,7 +332,8 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             const uint64_t per = total / ((uint64_t)s.eval_grid * kWarps * 2 + 1);
             C = 1024;
             while (C < kDefaultChunk && (uint64_t)C * 2 <= per) C *= 2;
-            while (C < kMaxChunk && (uint64_t)C * kCombineChunks < biggest) C *= 2;
+            const double want = std::pow(1.25 * (double)biggest, 2.0 / 3.0);
+            while (C < kMaxChunk && (double)C * 1.5 < want) C *= 2;
         }
         // chunk summaries are sized exactly by k_plan (PlanPool); these are
         // the per-chunk capacities of the first overflow re-run tier (x4).
@@ -416,8 +426,9 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     a.frames = s.frames.as<float2>();
     a.max_steps = 0xffffffffu;   // first pass: k_plan's exact buffers (checked at item end)
     a.max_frames = 0xffffffffu;
+    a.spill_frames = spill_frames(s.cur_chunk);
+    TRY(s.spill.ensure((size_t)s.eval_grid * kWarps * a.spill_frames * kFrameBytes, s.dev));
     a.spill = s.spill.as<float2>();
-    a.spill_frames = spill_frames();
     TRY(s.ovf.ensure(sizeof(uint32_t) * std::max<uint32_t>(nitems, 1), s.dev));
     a.ovf = s.ovf.as<uint32_t>();
     a.rec = s.rec.as<float>();
@@ -563,7 +574,10 @@ int rerun_overflowed(ltgp_engine* e, Shard& s) {
         int grid;
         EvalArgs a = s.eargs;
         if (worst) {
-            grid = std::max(1, std::min<int>(kRerunCtas, (int)((n + kWarps - 1) / kWarps)));
+            // worst-case spill is (C + 8) frames per warp: keep it within ~8 GB
+            const int mem_ctas = (int)std::max<uint64_t>(
+                1, (8ull << 30) / ((uint64_t)kWarps * (C + 8) * kFrameBytes));
+            grid = std::max(1, std::min<int>({kRerunCtas, mem_ctas, (int)((n + kWarps - 1) / kWarps)}));
             TRY(s.big_spill.ensure((size_t)grid * kWarps * (C + 8) * kFrameBytes, s.dev));
             a.spill = s.big_spill.as<float2>();
             a.spill_frames = C + 8;
