@@ -409,6 +409,8 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         pool.steps = s.steps.as<uint8_t>();
         pool.used = reinterpret_cast<unsigned long long*>(s.counters.as<uint32_t>() + kPoolCounters);
     }
+    pool.spill_frames = spill_frames(s.cur_chunk);
+    pool.adjusts = s.counters.as<uint32_t>() + 5;  // inline window adjusts join the statistics
     TRY(s.rec.ensure(sizeof(ltgp_record) * std::max<uint32_t>(ts.count, 1), s.dev));
     if (want_outs) TRY(s.outs.ensure(sizeof(float) * kLanes * std::max<uint32_t>(ts.count, 1), s.dev));
     CK(cudaMemsetAsync(s.counters.p, 0, kCounterBytes, s.st));
