@@ -19,6 +19,8 @@ def main():
     ap.add_argument("--check", type=int, default=2)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--chunk", type=int, default=0)
+    ap.add_argument("--cpu-trees", type=int, default=0,
+                    help="time the CPU oracle (evaluate_population, all host threads) on this many trees")
     a = ap.parse_args()
     n = a.nodes | 1
     t = time.perf_counter()
@@ -37,6 +39,22 @@ def main():
                   f"{st['combine_seconds']*1e3:.1f}) {tot*48/st['eval_seconds']/1e12:.3f} T GPops/s, chunks "
                   f"{st['last_chunks']}, reruns {st['last_fallback_items']}, exits {st['last_exits']}, "
                   f"adjusts {st['last_window_adjusts']}", flush=True)
+    if a.cpu_trees:  # the reference's CPU path (oracle port), one tree per thread as the reference does
+        from tests._oracle import load_oracle
+        o = load_oracle()
+        k = min(a.cpu_trees, a.trees)
+        offs = np.zeros(k, np.uint64)
+        sizes = np.full(k, n, np.uint64)
+        stride = (n + 15) // 16 * 16
+        buf = np.full(stride * k + 64, 0xFF, np.uint8)
+        for j in range(k):
+            offs[j] = j * stride
+            buf[j * stride:j * stride + n] = trees[j]
+        t = time.perf_counter()
+        o.evaluate_population(buf, offs, sizes, suite, threads=0)
+        dt = time.perf_counter() - t
+        print(f"cpu oracle: {k} trees x {n} nodes in {dt:.2f} s on {os.cpu_count()} threads: "
+              f"{k * n * 48 / dt / 1e12:.4f} T GPops/s", flush=True)
     if a.check:
         from tests._oracle import load_oracle, same_bits
         o = load_oracle()
