@@ -20,15 +20,16 @@ def main():
     ap.add_argument("--shards", type=int, default=1)
     ap.add_argument("--oracle", action="store_true")
     ap.add_argument("--grow", type=int, default=1, help="0: SPEC grow (runs collapse), 1: 50/50 grow (runs bloat)")
-    ap.add_argument("--dump", default="/tmp/c2_gpu.txt")
+    ap.add_argument("--dump", default="/tmp/c2_gpu.txt", help="generation dump path ('' for none)")
     a = ap.parse_args()
     with ltgp.Engine([0] * a.shards, node_limit=a.limit) as e:
         t = time.perf_counter()
-        r = e.run(a.pop, a.gens, a.limit, 7, a.seed, a.dump, a.grow)
+        r = e.run(a.pop, a.gens, a.limit, 7, a.seed, a.dump or None, a.grow)
         wall = time.perf_counter() - t
     print(f"engine: {r['generations']} gens, reason {r['reason']}, {r['nodes']} nodes, eval {r['eval_seconds']:.3f} s "
           f"({r['nodes'] * 48 / max(r['eval_seconds'], 1e-9) / 1e12:.3f} T GPops/s eval), wall {wall:.2f} s "
-          f"({r['nodes'] * 48 / wall / 1e9:.1f} G GPops/s end to end)", flush=True)
+          f"({r['nodes'] * 48 / wall / 1e9:.1f} G GPops/s end to end, {r['generations'] / wall * 3600:.0f} generations/hour)",
+          flush=True)
     if a.oracle:
         from tests._oracle import load_oracle
         o = load_oracle()
