@@ -119,10 +119,19 @@ int ltgp_evaluate_collect(ltgp_engine* e, ltgp_record* out, uint64_t* nodes);
 /* execute_generation (evolve.hpp:111-117): for every plan, crossover
    (genome.hpp:80-84) mum[0,ms) ++ dad[ds,de) ++ mum[me,n) on device, then
    evaluate the child. On success the children become the population
-   (double buffering, evolve.hpp:45). If any child would reach node_limit,
-   *size_limit_hit = 1 and the population is left unchanged. */
+   (double buffering, evolve.hpp:45). The run-ending outcomes leave the
+   population unchanged and are reported in *size_limit_hit (0 otherwise):
+   2 = MemoryBudgetExceeded, checked first, before anything is built: the
+   planned generation bytes (parents plus every child, child sizes from the
+   crossover algebra; evolve.hpp:89-93) exceed the budget set with
+   ltgp_set_memory_budget; 1 = SizeLimitHit, some child would reach
+   node_limit (evolve.hpp:102-104). */
 int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M,
                             ltgp_record* out, int* size_limit_hit);
+
+/* RunConfig::memory_budget_bytes (evolve.hpp:44): genome bytes a generation
+   may plan (parents + children); 0 (the default) disables the check. */
+int ltgp_set_memory_budget(ltgp_engine* e, uint64_t bytes);
 
 /* Genome bytes of slot idx (for dumps, to_text, parity). *size is always set. */
 int ltgp_download_genome(ltgp_engine* e, uint32_t idx, uint8_t* buf, uint64_t cap,

@@ -49,14 +49,17 @@ void ltgp_host_plan_generation(uint64_t seed, uint32_t M, const ltgp_record* pop
                                ltgp_plan* out);
 
 /* run() (run.hpp:33-36) on the engine: ramped init, generation-0
-   evaluation, plan/execute until max_generations or SizeLimitHit. Writes the
-   determinism dump (stats.hpp:104-107) to dump_path (NULL: none) and returns
-   generations completed (< 0: error, see ltgp_last_error()). grow_mode: 0 =
-   SPEC grow (uniform over the 255 primitives), 1 = 50/50 function-vs-terminal
-   grow (SPEC.md:148 open question; the variant whose runs bloat). */
+   evaluation, plan/execute until max_generations, SizeLimitHit or (with a
+   non-zero memory_budget = RunConfig::memory_budget_bytes) MemoryBudgetExceeded.
+   *reason: 0 MaxGenerations, 1 SizeLimitHit, 2 MemoryBudgetExceeded
+   (TerminationReason, evolve.hpp:34). Writes the determinism dump
+   (stats.hpp:104-107) to dump_path (NULL: none) and returns generations
+   completed (< 0: error, see ltgp_last_error()). grow_mode: 0 = SPEC grow
+   (uniform over the 255 primitives), 1 = 50/50 function-vs-terminal grow
+   (SPEC.md:148 open question; the variant whose runs bloat). */
 int64_t ltgp_host_run(ltgp_engine* e, uint32_t M, uint32_t max_generations, uint64_t node_limit,
-                      uint32_t k, uint64_t seed, int grow_mode, const char* dump_path, int* reason,
-                      uint64_t* nodes_evaluated, double* eval_seconds);
+                      uint32_t k, uint64_t seed, int grow_mode, uint64_t memory_budget,
+                      const char* dump_path, int* reason, uint64_t* nodes_evaluated, double* eval_seconds);
 
 #ifdef __cplusplus
 }

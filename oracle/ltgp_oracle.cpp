@@ -559,7 +559,8 @@ void orc_plan_generation(uint64_t seed, uint32_t M, const orc_record* pop, uint3
 // splice + evaluate into fixed child slots) until max_generations or the
 // first child reaching node_limit.
 int64_t orc_run(uint32_t M, uint32_t G, uint64_t node_limit, uint32_t k, uint64_t seed,
-                int threads, const char* dump_path, int* reason, uint64_t* nodes_evaluated, int grow_mode) {
+                int threads, const char* dump_path, int* reason, uint64_t* nodes_evaluated, int grow_mode,
+                uint64_t memory_budget) {
     Suite s;
     Rng srng(suite_seed(seed));
     make_suite(srng, s.in, s.tg, s.cs);
@@ -595,6 +596,19 @@ int64_t orc_run(uint32_t M, uint32_t G, uint64_t node_limit, uint32_t k, uint64_
     for (uint32_t gen = 1; gen <= G; ++gen) {
         for (uint32_t i = 0; i < M; ++i) { fit[i] = rec[i].fitness; size[i] = rec[i].size; }
         plan_generation(rng, M, fit.data(), size.data(), k, plans.data());
+        if (memory_budget) {  // planned_generation_bytes (evolve.hpp:89-93), checked before materializing
+            std::vector<uint64_t> cn(M);
+            parallel_for(M, threads, [&](uint32_t c, std::vector<Frame>&) {
+                const orc_plan& p = plans[c];
+                uint64_t ms, me, ds, de;
+                subtree_extent(pop[p.mum_index].data(), pop[p.mum_index].size(), p.mum_pt, &ms, &me);
+                subtree_extent(pop[p.dad_index].data(), pop[p.dad_index].size(), p.dad_pt, &ds, &de);
+                cn[c] = pop[p.mum_index].size() - (me - ms) + (de - ds);
+            });
+            uint64_t bytes = 0;
+            for (uint32_t i = 0; i < M; ++i) bytes += pop[i].size() + cn[i];
+            if (bytes > memory_budget) { *reason = 2; break; }
+        }
         std::atomic<int> hit{0};
         parallel_for(M, threads, [&](uint32_t c, std::vector<Frame>& st) {
             const orc_plan& p = plans[c];

@@ -90,10 +90,14 @@ void orc_plan_generation(uint64_t seed, uint32_t M, const orc_record* pop, uint3
    line per individual per generation, stats.hpp:104-107) into dump_path
    (NULL = none). Returns generations completed; *reason: 0 MaxGenerations,
    1 SizeLimitHit, 2 MemoryBudgetExceeded. grow_mode: 0 = SPEC grow (uniform
-   over the 255 primitives), 1 = 50/50 function-vs-terminal grow. */
+   over the 255 primitives), 1 = 50/50 function-vs-terminal grow.
+   memory_budget (RunConfig::memory_budget_bytes, evolve.hpp:44; 0 = off):
+   before a generation is materialized, planned_generation_bytes (parents
+   plus every planned child, child sizes from the crossover algebra;
+   evolve.hpp:89-93) must not exceed it. */
 int64_t orc_run(uint32_t M, uint32_t max_generations, uint64_t node_limit, uint32_t k,
                 uint64_t seed, int threads, const char* dump_path, int* reason,
-                uint64_t* nodes_evaluated, int grow_mode);
+                uint64_t* nodes_evaluated, int grow_mode, uint64_t memory_budget);
 
 #ifdef __cplusplus
 }

@@ -62,6 +62,7 @@ _CUDA_SIGS = {
     "ltgp_engine_create": (C.c_int, [C.POINTER(_Config), C.POINTER(_P)]),
     "ltgp_engine_destroy": (C.c_int, [_P]),
     "ltgp_set_suite": (C.c_int, [_P, _P, _P, _P]),
+    "ltgp_set_memory_budget": (C.c_int, [_P, C.c_uint64]),
     "ltgp_upload_population": (C.c_int, [_P, C.c_uint32, _P, _P]),
     "ltgp_upload_packed": (C.c_int, [_P, C.c_uint32, _P, C.c_uint64, _P, _P]),
     "ltgp_evaluate_packed": (C.c_int, [_P, C.c_uint32, _P, C.c_uint64, _P, _P, _P, _P]),
@@ -90,7 +91,7 @@ _HOST_SIGS = {
     "ltgp_host_ramped": (C.c_uint64, [C.c_uint64, C.c_uint32, C.c_uint64, C.c_int, C.c_int, _P,
                                       C.c_uint64, _P]),
     "ltgp_host_plan_generation": (None, [C.c_uint64, C.c_uint32, _P, C.c_uint32, _P]),
-    "ltgp_host_run": (C.c_int64, [_P, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint64, C.c_int,
+    "ltgp_host_run": (C.c_int64, [_P, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint64, C.c_int, C.c_uint64,
                                   C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_uint64),
                                   C.POINTER(C.c_double)]),
 }
@@ -371,12 +372,13 @@ class Engine:
         return p.value, f.value, n.value, st.value
 
     def run(self, M: int, generations: int, node_limit: int, k: int = 7, seed: int = 1,
-            dump_path: str | None = None, grow_mode: int = 0):
-        """run() (run.hpp:33-36) driven from C++ on this engine."""
+            dump_path: str | None = None, grow_mode: int = 0, memory_budget: int = 0):
+        """run() (run.hpp:33-36) driven from C++ on this engine; reason 0
+        MaxGenerations, 1 SizeLimitHit, 2 MemoryBudgetExceeded."""
         reason = C.c_int()
         nodes = C.c_uint64()
         secs = C.c_double()
-        done = host_lib().ltgp_host_run(self._h, M, generations, node_limit, k, seed, grow_mode,
+        done = host_lib().ltgp_host_run(self._h, M, generations, node_limit, k, seed, grow_mode, memory_budget,
                                         dump_path.encode() if dump_path else None,
                                         C.byref(reason), C.byref(nodes), C.byref(secs))
         if done < 0:

@@ -241,6 +241,7 @@ struct ltgp_engine {
     SuiteArgs suite;
     bool have_suite = false;
     uint32_t M = 0;
+    uint64_t memory_budget = 0;  // planned generation bytes allowed (0: no check)
     ltgp_stats stats;
     HostBuf staging;
 };
@@ -817,6 +818,12 @@ int ltgp_engine_destroy(ltgp_engine* e) {
     return 0;
 }
 
+int ltgp_set_memory_budget(ltgp_engine* e, uint64_t bytes) {
+    if (!e) { set_err("null engine"); return -1; }
+    e->memory_budget = bytes;
+    return 0;
+}
+
 int ltgp_set_suite(ltgp_engine* e, const float* in, const float* tg, const float* cs) {
     if (!e || !in || !tg || !cs) { set_err("null argument"); return -1; }
     for (int l = 0; l < 24; ++l) {
@@ -1124,10 +1131,18 @@ int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M, 
         if (qcount[g] && s.h_counters.as<uint32_t>()[3]) { set_err("malformed parent genome in extent scan"); return -1; }
     }
     tr.mark("extents");
-    // 2. SizeLimitHit (genome.hpp:71-84): child >= node_limit
+    // 2. MemoryBudgetExceeded (evolve.hpp:89-93): the
+    // generation's planned genome bytes (parents plus every child, sizes from
+    // the crossover algebra) over the budget, checked before materializing
+    if (e->memory_budget) {
+        uint64_t bytes = 0;
+        for (uint32_t c = 0; c < M; ++c) bytes += dir[c].size + csize[c];
+        if (bytes > e->memory_budget) { *size_limit_hit = 2; return 0; }
+    }
+    // 3. SizeLimitHit (genome.hpp:71-84): child >= node_limit
     for (uint32_t c = 0; c < M; ++c)
         if (csize[c] >= e->cfg.node_limit || csize[c] > 0xffffffffull) { *size_limit_hit = 1; return 0; }
-    // 3. children partitioned by bytes; splice into the other buffer
+    // 4. children partitioned by bytes; splice into the other buffer
     // (parents stay readable until every shard has spliced).
     std::vector<uint32_t> old_cur(G);
     for (int g = 0; g < G; ++g) old_cur[g] = e->shards[g].cur;

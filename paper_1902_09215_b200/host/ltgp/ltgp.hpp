@@ -156,7 +156,10 @@ struct ExecContext {     // evolve.hpp:95-100, plus the engine handle
     ltgp_engine* engine = nullptr;
 };
 
-struct ExecOutcome { bool size_limit_hit = false; };  // evolve.hpp:102-104
+struct ExecOutcome {  // evolve.hpp:102-104, plus the memory budget outcome
+    bool size_limit_hit = false;
+    bool memory_budget_exceeded = false;
+};
 
 inline bool fitness_better(float a, float b) {  // eval.hpp:90-94
     if (a != a) return false;

@@ -230,9 +230,11 @@ ExecOutcome execute_generation(std::span<const CrossoverPlan> plans, std::vector
     if (plans.size() != parents.size()) throw std::invalid_argument("one plan per child slot");
     std::vector<ltgp_record> rec(plans.size());
     int hit = 0;
+    check(ltgp_set_memory_budget(ctx.engine, ctx.config.memory_budget_bytes));
     check(ltgp_execute_generation(ctx.engine, plans.data(), static_cast<std::uint32_t>(plans.size()),
                                   rec.data(), &hit));
-    if (hit) return ExecOutcome{true};
+    if (hit == 2) return ExecOutcome{false, true};  // MemoryBudgetExceeded: nothing was built
+    if (hit) return ExecOutcome{true, false};
     children.resize(plans.size());
     for (std::size_t i = 0; i < plans.size(); ++i) {
         children[i].genome.release();  // device resident (ltgp_download_genome)
@@ -240,7 +242,7 @@ ExecOutcome execute_generation(std::span<const CrossoverPlan> plans, std::vector
     }
     ctx.gauge.add(static_cast<std::int64_t>(plans.size()));
     ctx.gauge.sub(static_cast<std::int64_t>(parents.size()));
-    return ExecOutcome{false};
+    return ExecOutcome{false, false};
 }
 
 }  // namespace ltgp
@@ -376,7 +378,8 @@ void ltgp_host_plan_generation(uint64_t seed, uint32_t M, const ltgp_record* rec
 
 // run.hpp:33-36 on the engine.
 int64_t ltgp_host_run(ltgp_engine* e, uint32_t M, uint32_t G, uint64_t node_limit, uint32_t k, uint64_t seed,
-                      int grow_mode, const char* dump_path, int* reason, uint64_t* nodes, double* eval_seconds) {
+                      int grow_mode, uint64_t memory_budget, const char* dump_path, int* reason, uint64_t* nodes,
+                      double* eval_seconds) {
     try {
         RunConfig cfg;
         cfg.population_size = M;
@@ -384,6 +387,7 @@ int64_t ltgp_host_run(ltgp_engine* e, uint32_t M, uint32_t G, uint64_t node_limi
         cfg.node_limit = node_limit;
         cfg.tournament_size = k;
         cfg.seed = seed;
+        cfg.memory_budget_bytes = memory_budget;
         validate(cfg);
         const TestSuite suite = make_suite(suite_seed(seed));
         Rng rng(seed);
@@ -417,6 +421,7 @@ int64_t ltgp_host_run(ltgp_engine* e, uint32_t M, uint32_t G, uint64_t node_limi
         for (uint32_t gen = 1; gen <= G; ++gen) {
             const auto plans = plan_generation(rng, pop, k);
             const ExecOutcome o = execute_generation(plans, pop, next, ctx);
+            if (o.memory_budget_exceeded) { *reason = 2; break; }  // TerminationReason (evolve.hpp:34)
             if (o.size_limit_hit) { *reason = 1; break; }
             std::swap(pop, next);
             check(ltgp_get_stats(e, &st));

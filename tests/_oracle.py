@@ -45,7 +45,7 @@ SIGS = {
     "orc_tournament_seq": (C.c_uint32, [C.c_uint64, C.c_uint32, P, C.c_uint32, C.c_uint32, P]),
     "orc_plan_generation": (None, [C.c_uint64, C.c_uint32, P, C.c_uint32, P]),
     "orc_run": (C.c_int64, [C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint64, C.c_int, C.c_char_p,
-                            C.POINTER(C.c_int), C.POINTER(C.c_uint64), C.c_int]),
+                            C.POINTER(C.c_int), C.POINTER(C.c_uint64), C.c_int, C.c_uint64]),
 }
 
 
@@ -142,10 +142,10 @@ class Oracle:
         self.lib.orc_plan_generation(seed, len(rec), _p(np.ascontiguousarray(rec, REC)), k, _p(out))
         return out
 
-    def run(self, M, G, node_limit, k=7, seed=1, threads=0, dump=None, grow_mode=0):
+    def run(self, M, G, node_limit, k=7, seed=1, threads=0, dump=None, grow_mode=0, memory_budget=0):
         reason, nodes = C.c_int(), C.c_uint64()
         done = self.lib.orc_run(M, G, node_limit, k, seed, threads, dump.encode() if dump else None,
-                                C.byref(reason), C.byref(nodes), grow_mode)
+                                C.byref(reason), C.byref(nodes), grow_mode, memory_budget)
         return {"generations": int(done), "reason": int(reason.value), "nodes": int(nodes.value)}
 
 

@@ -241,6 +241,26 @@ def test_run_size_limit_matches_oracle(oracle, tmp_path):
     assert (tmp_path / "a").read_bytes() == (tmp_path / "b").read_bytes()
 
 
+def test_run_memory_budget_matches_oracle(oracle, tmp_path):
+    """MemoryBudgetExceeded (evolve.hpp:44, :89-93): the engine's
+    run refuses the same generation as the oracle's (planned bytes from the
+    device's child sizes), with identical dumps, at 1 and 2 shards."""
+    from tests.test_oracle import budget_case
+    G = 40
+    full = tmp_path / "full.txt"
+    oracle.run(48, G, 10**9, 7, 1, 2, str(full), 1)
+    budget, g0 = budget_case(full.read_text(), G)
+    ref = tmp_path / "ref.txt"
+    ro = oracle.run(48, G, 10**9, 7, 1, 2, str(ref), 1, memory_budget=budget)
+    assert ro["reason"] == 2 and ro["generations"] == g0 - 1
+    for shards in (1, 2):
+        out = tmp_path / f"gpu{shards}.txt"
+        with ltgp.Engine([0] * shards, node_limit=10**9) as e:
+            r = e.run(48, G, 10**9, 7, 1, str(out), 1, memory_budget=budget)
+        assert r["reason"] == 2 and r["generations"] == g0 - 1
+        assert out.read_bytes() == ref.read_bytes()
+
+
 def test_config3_full_size_sampled(oracle, suite):
     """BASELINE config 3 at full size (4000 trees, 10^4..10^6 nodes): every
     record compared with the oracle (multi-threaded)."""

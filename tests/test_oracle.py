@@ -267,3 +267,39 @@ def test_run_size_limit(oracle):
     # node_limit=63, bloating run terminates with SizeLimitHit
     r = oracle.run(48, 500, 63, 7, 1, 1, None)
     assert r["reason"] == 1 and r["generations"] < 500
+
+
+def budget_case(dump_text, gens):
+    """From an unbudgeted run's dump: per-generation genome bytes T[g] and a
+    memory budget under which generation g0 is the first refused (its planned
+    bytes T[g0-1] + T[g0] exceed the budget, every earlier one fits)."""
+    T = [0] * (gens + 1)
+    for line in dump_text.splitlines():
+        g, _, size = line.split()[:3]
+        T[int(g)] += int(size)
+    planned = [T[g - 1] + T[g] for g in range(1, gens + 1)]
+    # the last generation (after the first) whose planned bytes set a new record
+    records = [g for g in range(2, gens + 1) if planned[g - 1] > max(planned[: g - 1])]
+    assert records, "no generation plans more bytes than all before it (the run does not bloat)"
+    g0 = records[-1]
+    return max(planned[: g0 - 1]), g0
+
+
+def test_run_memory_budget(oracle, tmp_path):
+    # SPEC.md:376, :395 / evolve.hpp:44, :89-93: with a memory budget the run
+    # stops with MemoryBudgetExceeded before materializing the first
+    # generation whose planned bytes (parents + children) exceed it; the
+    # generations before are unchanged
+    G = 40
+    full = tmp_path / "full.txt"
+    r = oracle.run(48, G, 10**9, 7, 1, 2, str(full), 1)
+    assert r["reason"] == 0 and r["generations"] == G
+    budget, g0 = budget_case(full.read_text(), G)
+    assert g0 > 1
+    cut = tmp_path / "cut.txt"
+    rb = oracle.run(48, G, 10**9, 7, 1, 2, str(cut), 1, memory_budget=budget)
+    assert rb["reason"] == 2 and rb["generations"] == g0 - 1
+    lines = full.read_text().splitlines()
+    assert cut.read_text().splitlines() == lines[: 48 * g0]
+    # budget 0 disables the check
+    assert oracle.run(48, G, 10**9, 7, 1, 2, None, 1, memory_budget=0)["reason"] == 0
