@@ -70,6 +70,23 @@ typedef struct {
     uint32_t kernel_launches;   /* engine kernels launched by the last call */
 } ltgp_stats;
 
+/* Generation statistics of the current population (GenerationStats,
+   stats.hpp:14-27; best_index / convergence, stats.hpp:36-40), reduced on the
+   device from the records of the last evaluation. */
+typedef struct {
+    uint32_t best_index;    /* first slot holding the best fitness (NaN is worst) */
+    float best_fitness;
+    int32_t best_hits;
+    uint32_t best_size;
+    uint32_t best_depth;
+    uint32_t convergence;   /* slots whose fitness is bit-equal to the best's */
+    uint32_t max_size;
+    uint32_t pad;
+    uint64_t sum_size;      /* mean_size = sum_size / M (exact) */
+    uint64_t sum_depth;     /* mean_depth = sum_depth / M (exact) */
+    double sum_fitness;     /* in slot order, double accumulation (mean_fitness = sum / M) */
+} ltgp_gen_stats;
+
 const char* ltgp_last_error(void);
 const char* ltgp_version(void);
 
@@ -128,6 +145,10 @@ int ltgp_evaluate_collect(ltgp_engine* e, ltgp_record* out, uint64_t* nodes);
    node_limit (evolve.hpp:102-104). */
 int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M,
                             ltgp_record* out, int* size_limit_hit);
+
+/* Generation statistics of the current population (after an evaluation or
+   execute_generation): no host pass over the records. */
+int ltgp_generation_stats(ltgp_engine* e, ltgp_gen_stats* out);
 
 /* RunConfig::memory_budget_bytes (evolve.hpp:44): genome bytes a generation
    may plan (parents + children); 0 (the default) disables the check. */

@@ -30,6 +30,10 @@ CONSTANTS = 250
 MAX_SHARDS = 16
 
 RECORD_DTYPE = np.dtype([("fitness", "<f4"), ("hits", "<i4"), ("size", "<u4"), ("depth", "<u4")])
+GEN_STATS_DTYPE = np.dtype([("best_index", "<u4"), ("best_fitness", "<f4"), ("best_hits", "<i4"),
+                            ("best_size", "<u4"), ("best_depth", "<u4"), ("convergence", "<u4"),
+                            ("max_size", "<u4"), ("pad", "<u4"), ("sum_size", "<u8"), ("sum_depth", "<u8"),
+                            ("sum_fitness", "<f8")])
 PLAN_DTYPE = np.dtype([("mum_index", "<u4"), ("dad_index", "<u4"), ("mum_pt", "<u4"), ("dad_pt", "<u4")])
 
 
@@ -63,6 +67,7 @@ _CUDA_SIGS = {
     "ltgp_engine_destroy": (C.c_int, [_P]),
     "ltgp_set_suite": (C.c_int, [_P, _P, _P, _P]),
     "ltgp_set_memory_budget": (C.c_int, [_P, C.c_uint64]),
+    "ltgp_generation_stats": (C.c_int, [_P, _P]),
     "ltgp_upload_population": (C.c_int, [_P, C.c_uint32, _P, _P]),
     "ltgp_upload_packed": (C.c_int, [_P, C.c_uint32, _P, C.c_uint64, _P, _P]),
     "ltgp_evaluate_packed": (C.c_int, [_P, C.c_uint32, _P, C.c_uint64, _P, _P, _P, _P]),
@@ -308,6 +313,14 @@ class Engine:
         _check(self._lib.ltgp_evaluate_packed(self._h, M, _ptr(buf), buf.nbytes, _ptr(offsets), _ptr(sizes),
                                               _ptr(rec), _ptr(outs)))
         return (rec, outs) if outputs else rec
+
+    def generation_stats(self) -> dict:
+        """GenerationStats of the current population (stats.hpp:14-40), reduced
+        on the device: best slot / fitness / hits / size / depth, convergence,
+        max size, exact size and depth sums, fitness sum in slot order."""
+        out = np.zeros(1, GEN_STATS_DTYPE)
+        _check(self._lib.ltgp_generation_stats(self._h, _ptr(out)))
+        return {k: out[k][0].item() for k in GEN_STATS_DTYPE.names if k != "pad"}
 
     def population_size(self) -> int:
         return int(self._lib.ltgp_population_size(self._h))

@@ -214,12 +214,15 @@ struct Shard {
     // crossover scratch
     DevBuf plans, ext, csize, coff, dir;
     HostBuf h_csize, h_coff, h_dir;
+    DevBuf gstats;      // generation statistics scratch (GenStatsDev + best bits)
+    HostBuf h_gstats;
     void release() {
         set[0].release(); set[1].release(); scratch.release();
         for (DevBuf* b : {&items, &ctrees, &hdr, &steps, &frames, &dframes, &segs, &spill, &counters,
                           &rec, &outs, &plans, &ext, &csize, &coff, &dir, &big_steps[0], &big_frames[0],
                           &big_steps[1], &big_frames[1], &rerun_items[0], &rerun_slot[0], &rerun_items[1],
-                          &rerun_slot[1], &ovf, &big_spill}) b->release();
+                          &rerun_slot[1], &ovf, &big_spill, &gstats}) b->release();
+        h_gstats.release();
         h_items.release(); h_ctrees.release(); h_counters.release();
         h_csize.release(); h_coff.release(); h_dir.release();
         for (auto& b : xspill) b.release();
@@ -815,6 +818,75 @@ int ltgp_engine_destroy(ltgp_engine* e) {
     }
     e->staging.release();
     delete e;
+    return 0;
+}
+
+int ltgp_generation_stats(ltgp_engine* e, ltgp_gen_stats* out) {
+    if (!e || !out) { set_err("null argument"); return -1; }
+    if (!e->M) { set_err("no population"); return -1; }
+    const size_t kS = sizeof(GenStatsDev);
+    // pass 1 per shard: best slot, max size, sums
+    for (Shard& s : e->shards) {
+        if (!s.count) continue;
+        CK(cudaSetDevice(s.dev));
+        TRY(s.gstats.ensure(kS + 16, s.dev));
+        TRY(s.h_gstats.ensure(kS + 16));
+        k_gen_stats<<<1, 1024, 0, s.st>>>(s.rec.as<float>(), s.count, s.gstats.as<GenStatsDev>(), nullptr);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(s.h_gstats.p, s.gstats.p, kS, cudaMemcpyDeviceToHost, s.st));
+    }
+    ltgp_gen_stats r{};
+    float bf = 0.0f;
+    uint32_t bi = 0xffffffffu, bbits = 0;
+    const Shard* bs = nullptr;
+    auto better = [](float fa, uint32_t ia, float fb, uint32_t ib) {  // fitness_better + lower slot
+        if (fa != fa) return (fb != fb) && ia < ib;
+        if (fb != fb) return true;
+        return fa < fb || (fa == fb && ia < ib);
+    };
+    for (Shard& s : e->shards) {  // shards hold consecutive slot ranges: slot order
+        if (!s.count) continue;
+        CK(cudaSetDevice(s.dev));
+        CK(cudaStreamSynchronize(s.st));
+        const GenStatsDev g = *s.h_gstats.as<GenStatsDev>();
+        float f;
+        std::memcpy(&f, &g.best_bits, 4);
+        const uint32_t slot = s.first + g.best_slot;
+        if (bi == 0xffffffffu || better(f, slot, bf, bi)) { bf = f; bi = slot; bbits = g.best_bits; bs = &s; }
+        r.max_size = std::max(r.max_size, g.max_size);
+        r.sum_size += g.sum_size;
+        r.sum_depth += g.sum_depth;
+        r.sum_fitness += g.sum_fitness;
+    }
+    // the best record, then pass 2: convergence against the global best's bits
+    {
+        ltgp_record br;
+        CK(cudaSetDevice(bs->dev));
+        CK(cudaMemcpy(&br, bs->rec.as<ltgp_record>() + (bi - bs->first), sizeof br, cudaMemcpyDeviceToHost));
+        r.best_index = bi;
+        r.best_fitness = br.fitness;
+        r.best_hits = br.hits;
+        r.best_size = br.size;
+        r.best_depth = br.depth;
+    }
+    for (Shard& s : e->shards) {
+        if (!s.count) continue;
+        CK(cudaSetDevice(s.dev));
+        uint32_t* hb = reinterpret_cast<uint32_t*>(s.h_gstats.as<uint8_t>() + kS);
+        *hb = bbits;
+        uint32_t* db = reinterpret_cast<uint32_t*>(s.gstats.as<uint8_t>() + kS);
+        CK(cudaMemcpyAsync(db, hb, 4, cudaMemcpyHostToDevice, s.st));
+        k_gen_stats<<<1, 1024, 0, s.st>>>(s.rec.as<float>(), s.count, s.gstats.as<GenStatsDev>(), db);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(s.h_gstats.p, s.gstats.p, kS, cudaMemcpyDeviceToHost, s.st));
+    }
+    for (Shard& s : e->shards) {
+        if (!s.count) continue;
+        CK(cudaSetDevice(s.dev));
+        CK(cudaStreamSynchronize(s.st));
+        r.convergence += s.h_gstats.as<GenStatsDev>()->convergence;
+    }
+    *out = r;
     return 0;
 }
 

@@ -53,3 +53,23 @@ def test_no_gpu_fails_loudly():
         pytest.skip("GPU present")
     with pytest.raises(ltgp.EngineError):
         ltgp.Engine([0])
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """The ctypes/numpy views of ltgp_record and ltgp_gen_stats have the C
+    layout (offsets compiled from include/ltgp_cuda.h)."""
+    import subprocess
+    import paper_1902_09215_b200 as ltgp
+    src = tmp_path / "layout.c"
+    src.write_text(
+        '#include <stddef.h>\n#include <stdio.h>\n#include "ltgp_cuda.h"\n'
+        'int main(void){printf("%zu %zu %zu %zu %zu\\n", sizeof(ltgp_record), sizeof(ltgp_gen_stats),'
+        ' offsetof(ltgp_gen_stats, convergence), offsetof(ltgp_gen_stats, sum_size),'
+        ' offsetof(ltgp_gen_stats, sum_fitness)); return 0;}\n')
+    exe = tmp_path / "layout"
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    subprocess.run(["gcc", "-I", inc, str(src), "-o", str(exe)], check=True)
+    got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    g = ltgp.GEN_STATS_DTYPE
+    assert got == [ltgp.RECORD_DTYPE.itemsize, g.itemsize, g.fields["convergence"][1], g.fields["sum_size"][1],
+                   g.fields["sum_fitness"][1]]

@@ -261,6 +261,54 @@ def test_run_memory_budget_matches_oracle(oracle, tmp_path):
         assert out.read_bytes() == ref.read_bytes()
 
 
+def host_generation_stats(rec):
+    """GenerationStats (stats.hpp:14-40) from records, on the host: best =
+    first slot of the best fitness (NaN worst), convergence = bit-equal
+    fitness, fitness summed in slot order in double."""
+    f = rec["fitness"]
+    order = sorted(range(len(f)), key=lambda i: (np.isnan(f[i]), f[i] if not np.isnan(f[i]) else 0.0, i))
+    b = order[0]
+    s = 0.0
+    for v in f:
+        s += float(v)
+    return {"best_index": b, "best_fitness": float(f[b]), "best_hits": int(rec["hits"][b]),
+            "best_size": int(rec["size"][b]), "best_depth": int(rec["depth"][b]),
+            "convergence": int((f.view(np.uint32) == f[b:b + 1].view(np.uint32)[0]).sum()),
+            "max_size": int(rec["size"].max()), "sum_size": int(rec["size"].astype(np.uint64).sum()),
+            "sum_depth": int(rec["depth"].astype(np.uint64).sum()), "sum_fitness": s}
+
+
+def test_generation_stats_on_device(oracle, suite):
+    """ltgp_generation_stats equals the host reduction of the records: ties on
+    the best fitness (duplicated genomes), NaN fitness, 1 and 2 shards."""
+    gs = [np.array([MUL, 5 + 249] * 2000 + [X], np.uint8)] * 3            # NaN fitness
+    gs += [np.array([SUB, MUL, X, X, X], np.uint8)] * 5                   # ties, convergence 5
+    gs += [ltgp.random_tree_of_size(900 + k, 201 + 2 * k) for k in range(40)]
+    gs += [np.array([SUB, MUL, X, X, X], np.uint8)] * 2
+    for shards in (1, 2):
+        with ltgp.Engine([0] * shards, node_limit=10**9) as e:
+            e.set_suite(*suite)
+            e.upload_population(gs)
+            rec = e.evaluate_population()
+            got = e.generation_stats()
+        exp = host_generation_stats(rec)
+        fit = got.pop("sum_fitness"), exp.pop("sum_fitness")
+        assert got == exp or (np.isnan(got["best_fitness"]) and np.isnan(exp["best_fitness"]))
+        assert fit[0] == fit[1] or (np.isnan(fit[0]) and np.isnan(fit[1]))
+    # after a generation on device (children never leave the GPU)
+    with ltgp.Engine([0], node_limit=10**9) as e:
+        e.set_suite(*suite)
+        e.upload_population(gs)
+        rec0 = e.evaluate_population()
+        plans = ltgp.plan_generation(3, rec0, 7)
+        rec1, hit = e.execute_generation(plans)
+        assert not hit
+        got = e.generation_stats()
+    exp = host_generation_stats(rec1)
+    got.pop("sum_fitness"), exp.pop("sum_fitness")
+    assert got == exp or np.isnan(exp["best_fitness"])
+
+
 def test_config3_full_size_sampled(oracle, suite):
     """BASELINE config 3 at full size (4000 trees, 10^4..10^6 nodes): every
     record compared with the oracle (multi-threaded)."""
