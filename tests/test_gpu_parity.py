@@ -369,3 +369,46 @@ def test_config2_bloating_run_matches_oracle(oracle, tmp_path):
     assert r["generations"] == g["generations"] == 100
     assert r["nodes"] == g["nodes"]
     assert (tmp_path / "a").read_bytes() == (tmp_path / "b").read_bytes()
+
+
+@pytest.mark.parametrize("round_", range(int(os.environ.get("LTGP_FUZZ_ROUNDS", "3"))))
+def test_randomized_populations(oracle, suite, round_):
+    """Randomized sweep: mixed shapes (Remy, uniform splits, ramped
+    half-and-half, left/right chains), random sizes and chunk lengths, the
+    resident and the streamed path; every record and per-case output equal
+    to the oracle's."""
+    rng = np.random.default_rng(1000 + round_)
+    genomes = []
+    for k in range(60):
+        kind = rng.integers(0, 5)
+        n = int(rng.integers(1, 40000)) | 1
+        if kind == 0:
+            genomes.append(ltgp.remy_tree(int(rng.integers(1 << 30)), n))
+        elif kind == 1:
+            genomes.append(ltgp.random_tree_of_size(int(rng.integers(1 << 30)), n))
+        elif kind == 2:
+            genomes += ltgp.ramped_half_and_half(int(rng.integers(1 << 30)), 2)
+        elif kind == 3:  # left chain: op op ... op leaf leaf ... leaf
+            m = n // 2
+            ops = rng.integers(0, 4, m).astype(np.uint8)
+            leaves = rng.integers(4, 255, m + 1).astype(np.uint8)
+            genomes.append(np.concatenate([ops, leaves]))
+        else:  # right chain: op leaf op leaf ... leaf
+            m = n // 2
+            g = np.empty(2 * m + 1, np.uint8)
+            g[0:2 * m:2] = rng.integers(0, 4, m)
+            g[1:2 * m:2] = rng.integers(4, 255, m)
+            g[-1] = 4
+            genomes.append(g)
+    chunk = int(rng.choice([0, 64, 256, 1024, 4096, 16384]))
+    buf, offs, sizes = pack(genomes)
+    exp = oracle.evaluate_population(buf, offs, sizes, suite, threads=0)
+    with engine(suite, chunk=chunk) as e:
+        e.upload_population(genomes)
+        rec, outs = e.evaluate_outputs()
+        rec_s, outs_s = e.evaluate_packed(buf, offs, sizes, outputs=True)
+    assert_records_equal(rec, exp)
+    assert rec_s.tobytes() == rec.tobytes() and same_bits(outs_s, outs)
+    for k, g in enumerate(genomes):
+        o, _ = oracle.eval_batch(g, suite[0], suite[2])
+        assert same_bits(outs[k], o), f"tree {k} (size {g.size}, chunk {chunk})"
