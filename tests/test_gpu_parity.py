@@ -412,3 +412,48 @@ def test_randomized_populations(oracle, suite, round_):
     for k, g in enumerate(genomes):
         o, _ = oracle.eval_batch(g, suite[0], suite[2])
         assert same_bits(outs[k], o), f"tree {k} (size {g.size}, chunk {chunk})"
+
+
+def test_error_behaviour_and_edge_cases(oracle, suite):
+    """The reference's error conventions through the ABI: malformed genomes
+    (stack underflow / leftover values), out-of-range plans and crossover
+    points, a missing suite and misaligned packed offsets are errors (status
+    < 0 with a message, no crash); single-node trees and one-tree populations
+    evaluate normally, including on the streamed path."""
+    with engine(suite) as e:
+        for bad in ([ADD, X], [X, X], [ADD, X, X, X], [DIV]):
+            e.upload_population([np.array(bad, np.uint8)])
+            with pytest.raises(ltgp.EngineError, match="malformed"):
+                e.evaluate_population()
+        big_bad = np.concatenate([ltgp.remy_tree(5, 30001), np.array([X], np.uint8)])  # a leftover value
+        e.upload_population([big_bad])
+        with pytest.raises(ltgp.EngineError, match="malformed"):
+            e.evaluate_population()
+        # engine still usable afterwards
+        one = [np.array([5 + 17], np.uint8)]
+        e.upload_population(one)
+        rec = e.evaluate_population()
+        assert rec["size"][0] == 1 and rec["depth"][0] == 1
+        buf, offs, sizes = pack(one)
+        assert e.evaluate_packed(buf, offs, sizes).tobytes() == rec.tobytes()
+        # crossover plans
+        gs = [ltgp.random_tree_of_size(k, 101) for k in range(4)]
+        e.upload_population(gs)
+        e.evaluate_population()
+        plans = np.zeros(4, ltgp.PLAN_DTYPE)
+        plans["mum_index"] = [0, 1, 2, 7]
+        with pytest.raises(ltgp.EngineError, match="outside the population"):
+            e.execute_generation(plans)
+        plans["mum_index"] = [0, 1, 2, 3]
+        plans["mum_pt"] = [0, 1, 2, 101]
+        with pytest.raises(ltgp.EngineError, match="out of range"):
+            e.execute_generation(plans)
+        # misaligned packed offsets
+        b2, o2, s2 = pack(gs)
+        o2[1] += 1
+        with pytest.raises(ltgp.EngineError, match="16-aligned"):
+            e.evaluate_packed(b2, o2, s2)
+    with ltgp.Engine([0], node_limit=10**6) as e:
+        e.upload_population([np.array([X], np.uint8)])
+        with pytest.raises(ltgp.EngineError, match="set_suite"):
+            e.evaluate_population()
