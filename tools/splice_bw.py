@@ -1,6 +1,6 @@
 """Device crossover bandwidth: run the engine's run() for G generations (50/50
 grow, so trees bloat), then time further generations driven from Python and
-report the extent scan + splice device time (ltgp_stats.splice_seconds) per
+report the splice kernel's device time (ltgp_stats.splice_seconds) per
 generation against the bytes the splice moves (children written + the same
 bytes read from parents: 2 B/node)."""
 import os
@@ -22,5 +22,5 @@ with ltgp.Engine([0], node_limit=2**62) as e:
         st = e.stats()
         n = int(rec["size"].sum())
         s = st["splice_seconds"]
-        print(f"generation +{g}: children {n} nodes (mean {n / 4000:.0f}); extents + splice {s * 1e3:.3f} ms: "
+        print(f"generation +{g}: children {n} nodes (mean {n / 4000:.0f}); splice {s * 1e3:.3f} ms: "
               f"{2 * n / s / 1e9:.0f} GB/s of 2 B/node; evaluation {st['eval_seconds'] * 1e3:.3f} ms", flush=True)
