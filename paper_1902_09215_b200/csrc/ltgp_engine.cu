@@ -351,13 +351,16 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         std::vector<CombineTree> ctrees;
         s.slice_items.assign(G + 1, 0);
         uint32_t nch = 0;
+        all.reserve(ts.count + 64);
         for (uint32_t g = 0; g < G; ++g) {
             s.slice_items[g] = (uint32_t)all.size();
-            std::vector<Item> whole;
+            // whole trees largest first for load balance: by log2(size)
+            // buckets, descending (linear; stable within a bucket)
+            uint32_t bcount[33] = {};
             for (uint32_t t = tb[g]; t < tb[g + 1]; ++t) {
                 const uint32_t n = ts.h_size[t];
                 if (n <= C) {
-                    whole.push_back({t, kWholeTree, 0, n});
+                    ++bcount[32 - __builtin_clz(n)];
                     continue;
                 }
                 const uint32_t k = (n + C - 1) / C;
@@ -365,14 +368,23 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
                 for (uint32_t j = 0; j < k; ++j) all.push_back({t, nch + j, j * C, std::min(n, (j + 1) * C)});
                 nch += k;
             }
-            std::stable_sort(whole.begin(), whole.end(),
-                             [](const Item& x, const Item& y) { return x.hi > y.hi; });
-            all.insert(all.end(), whole.begin(), whole.end());
+            uint32_t bstart[33];
+            uint32_t pos = (uint32_t)all.size();
+            for (int b = 32; b >= 0; --b) {
+                bstart[b] = pos;
+                pos += bcount[b];
+            }
+            all.resize(pos);
+            for (uint32_t t = tb[g]; t < tb[g + 1]; ++t) {
+                const uint32_t n = ts.h_size[t];
+                if (n <= C) all[bstart[32 - __builtin_clz(n)]++] = Item{t, kWholeTree, 0, n};
+            }
         }
         s.slice_items[G] = (uint32_t)all.size();
         const uint32_t nitems = (uint32_t)all.size();
-        // the pinned staging buffers are reused: wait for older copies
-        CK(cudaStreamSynchronize(s.st));
+        // the pinned staging buffers are reused: wait for their last copies
+        // (not for the whole stream: a splice may still be running)
+        CK(cudaEventSynchronize(s.ev[7]));
         TRY(s.h_items.ensure(sizeof(Item) * std::max<uint32_t>(nitems, 1)));
         std::copy(all.begin(), all.end(), s.h_items.as<Item>());
         TRY(s.items.ensure(sizeof(Item) * std::max<uint32_t>(nitems, 1), s.dev));
@@ -394,6 +406,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         s.items_for = &ts;
         s.items_version = ts.version;
         s.items_slices = tb;
+        CK(cudaEventRecord(s.ev[7], s.st));  // h_items / h_ctrees copies issued
     }
     const uint32_t nitems = s.last_items, nct = s.last_ctrees, nch = s.last_chunks;
     // chunk-summary pool (k_plan claims every chunk's exact summary): an
@@ -1247,23 +1260,23 @@ int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M, 
         CK(cudaMemcpyAsync(ts.off.p, ts.h_off.data(), sizeof(uint64_t) * ts.count, cudaMemcpyHostToDevice, s.st));
         CK(cudaMemcpyAsync(ts.size.p, ts.h_size.data(), sizeof(uint32_t) * ts.count, cudaMemcpyHostToDevice, s.st));
     }
-    for (int g = 0; g < G; ++g) {
-        Shard& s = e->shards[g];
-        CK(cudaSetDevice(s.dev));
-        CK(cudaStreamSynchronize(s.st));  // all splices done: parents may be dropped
+    // no sync here: each shard evaluates its children on the stream that
+    // spliced them, and a parent arena is overwritten only by the next
+    // generation's splice, after this generation's collect has synchronised
+    // every shard (the splice reads parents on other shards through P2P)
+    for (int g = 0; g < G; ++g) e->shards[g].cur = 1 - old_cur[g];
+    tr.mark("splice");
+    // 5. evaluate the children
+    TRY(ltgp_evaluate_launch(e));
+    tr.mark("eval launch");
+    TRY(ltgp_evaluate_collect(e, out, nullptr));
+    for (Shard& s : e->shards)
         if (s.count) {
             float ms = 0.0f;
             CK(cudaEventElapsedTime(&ms, s.ev[2], s.ev[3]));
             splice_ms = std::max(splice_ms, ms);
         }
-    }
-    for (int g = 0; g < G; ++g) e->shards[g].cur = 1 - old_cur[g];
     e->stats.splice_seconds = splice_ms * 1e-3;
-    tr.mark("splice");
-    // 4. evaluate the children
-    TRY(ltgp_evaluate_launch(e));
-    tr.mark("eval launch");
-    TRY(ltgp_evaluate_collect(e, out, nullptr));
     tr.mark("eval collect");
     return 0;
 }
