@@ -33,7 +33,7 @@ constexpr int kWindow = 20;          // shared stack window frames per warp
 constexpr uint32_t kDefaultChunk = 16384;
 constexpr uint32_t kMaxSteps = 1024;
 constexpr uint32_t kMaxFrames = 256;
-constexpr uint32_t kMaxChunk = 524288;     // automatic chunk length ceiling
+constexpr uint32_t kMaxChunk = 1048576;    // automatic chunk length ceiling
 constexpr uint32_t kPlanWarpChunk = 32768; // chunk length from which k_plan_warp plans (a warp per item)
 constexpr uint32_t kSpillFrames = 1024;  // per warp; items that need more are re-run
 constexpr int kRerunCtas = 8;
@@ -324,8 +324,8 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         // warp per tree; more chunks cost combine work), 1024..16384 nodes;
         // and, for huge trees, long enough to balance one item's scan latency
         // (~C / 13e6 s) against the largest tree's sequential combine (~N/C
-        // chunks x 1.6 sqrt(C) spine steps x ~60 ns): C ~ (1.25 N)^(2/3),
-        // up to kMaxChunk (1e7 nodes: 65536; 4e8 nodes: 524288)
+        // chunks x 1.6 sqrt(C) spine steps x ~60 ns): C >= (1.25 N)^(2/3),
+        // up to kMaxChunk (1e7 nodes: 65536; 4e8 nodes: 1048576)
         uint32_t C = e->chunk;
         if (!e->chunk_fixed) {
             uint64_t total = 0, biggest = 0;
@@ -337,7 +337,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             C = 1024;
             while (C < kDefaultChunk && (uint64_t)C * 2 <= per) C *= 2;
             const double want = std::pow(1.25 * (double)biggest, 2.0 / 3.0);
-            while (C < kMaxChunk && (double)C * 1.5 < want) C *= 2;
+            while (C < kMaxChunk && (double)C < want) C *= 2;
         }
         // chunk summaries are sized exactly by k_plan (PlanPool); these are
         // the per-chunk capacities of the first overflow re-run tier (x4).
