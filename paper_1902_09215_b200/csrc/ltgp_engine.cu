@@ -320,8 +320,10 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     tb[G] = ts.count;
     if (s.items_for != &ts || s.items_version != ts.version || s.items_slices != tb) {
         // chunk length: the configured one, or sized so the persistent grid
-        // gets >= ~2 items per warp (small populations must not wait on one
-        // warp per tree; more chunks cost combine work), 1024..16384 nodes;
+        // gets >= ~1 item per warp (small populations must not wait on one
+        // warp per tree; more, shorter items cost per-item planning, exits
+        // and combine work: a 15.6M-node evolved population is 13% faster at
+        // 2048 than at 1024), 1024..16384 nodes;
         // and, for huge trees, long enough to balance one item's scan latency
         // (~C / 13e6 s) against the largest tree's sequential combine (~N/C
         // chunks x 1.6 sqrt(C) spine steps x ~60 ns): C >= (1.25 N)^(2/3),
@@ -333,7 +335,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
                 total += ts.h_size[t];
                 biggest = std::max<uint64_t>(biggest, ts.h_size[t]);
             }
-            const uint64_t per = total / ((uint64_t)s.eval_grid * kWarps * 2 + 1);
+            const uint64_t per = total / ((uint64_t)s.eval_grid * kWarps + 1);
             C = 1024;
             while (C < kDefaultChunk && (uint64_t)C * 2 <= per) C *= 2;
             const double want = std::pow(1.25 * (double)biggest, 2.0 / 3.0);
