@@ -34,7 +34,6 @@ constexpr uint32_t kDefaultChunk = 16384;
 constexpr uint32_t kMaxSteps = 1024;
 constexpr uint32_t kMaxFrames = 256;
 constexpr uint32_t kMaxChunk = 1048576;    // automatic chunk length ceiling
-constexpr uint32_t kPlanWarpChunk = 32768; // chunk length from which k_plan_warp plans (a warp per item)
 constexpr uint32_t kSpillFrames = 1024;  // per warp; items that need more are re-run
 constexpr int kRerunCtas = 8;
 
@@ -298,12 +297,6 @@ int init_shard(ltgp_engine* e, Shard& s) {
     return 0;
 }
 
-uint32_t ts_max_size(const TreeSet& ts) {
-    uint32_t m = 0;
-    for (uint32_t t = 0; t < ts.count; ++t) m = std::max(m, ts.h_size[t]);
-    return m;
-}
-
 // Evaluate every tree of `ts` on shard s: records (and optional per-case
 // outputs) land in rec/outs. Asynchronous on s.st.
 //
@@ -510,16 +503,12 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             DEBUG_SYNC(X, "k_decode");
             ++launches;
         }
-        // k_plan (a thread per item) is latency-bound on its longest item,
-        // k_plan_warp (a warp per item) throughput-bound on the total:
-        // ~3.6e-7 s per packet of the longest item vs ~2.7e-11 s per packet in
-        // all (config 3: thread 0.4 ms vs warp 1.6 ms; an evolved 15.6M-node
-        // population: warp 48 us faster); deep Remy chunks (>= 32768 nodes)
-        // diverge too much for the thread variant
-        static const int plan_mode = std::getenv("LTGP_PLAN") ? std::atoi(std::getenv("LTGP_PLAN")) : -1;
-        const uint64_t longest = std::min<uint64_t>(s.cur_chunk, ts_max_size(ts)) / 16 + 1;
-        const bool plan_warp = plan_mode >= 0 ? plan_mode == 1
-                                              : s.cur_chunk >= kPlanWarpChunk || packets < longest * 13300;
+        // k_plan_warp (a warp per item, lane-parallel replay between window
+        // adjustments) beats k_plan (a thread per item) on every measured
+        // population (config 3: 14.13 vs 14.20 ms per evaluation; an evolved
+        // 15.6M-node population: 0.66 vs 0.72 ms); LTGP_PLAN=0 selects k_plan
+        static const int plan_mode = std::getenv("LTGP_PLAN") ? std::atoi(std::getenv("LTGP_PLAN")) : 1;
+        const bool plan_warp = plan_mode != 0;
         if (ni && plan_warp) {  // a warp per item
             k_plan_warp<<<(ni + 3) / 4, 128, 0, X>>>(s.items.as<Item>() + i0, ni, ts.off.as<uint64_t>(),
                                                     reinterpret_cast<uint8_t*>(dec), ts.meta.as<uint32_t>(),

@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--grow", type=int, default=1, help="0: SPEC grow (runs collapse), 1: 50/50 grow (runs bloat)")
     ap.add_argument("--dump", default="/tmp/c2_gpu.txt", help="generation dump path ('' for none)")
     a = ap.parse_args()
+    if a.oracle and not a.dump:
+        ap.error("--oracle compares generation dumps: give --dump a path")
     with ltgp.Engine([0] * a.shards, node_limit=a.limit) as e:
         t = time.perf_counter()
         r = e.run(a.pop, a.gens, a.limit, 7, a.seed, a.dump or None, a.grow)
