@@ -67,6 +67,7 @@ typedef struct {
     uint64_t last_fallback_items; /* items re-run with worst-case capacities */
     uint64_t last_exits;        /* packets the fast path handed to the checked / window path */
     uint64_t last_window_adjusts; /* of which needed a stack window spill or refill */
+    uint64_t last_spine_steps;  /* spine steps the chunk summaries of the last evaluation hold */
     uint32_t kernel_launches;   /* engine kernels launched by the last call */
 } ltgp_stats;
 

@@ -52,7 +52,8 @@ class _Stats(C.Structure):
                 ("splice_seconds", C.c_double), ("gather_seconds", C.c_double),
                 ("arena_high_water", C.c_uint64), ("last_chunks", C.c_uint64),
                 ("last_fallback_items", C.c_uint64), ("last_exits", C.c_uint64),
-                ("last_window_adjusts", C.c_uint64), ("kernel_launches", C.c_uint32)]
+                ("last_window_adjusts", C.c_uint64), ("last_spine_steps", C.c_uint64),
+                ("kernel_launches", C.c_uint32)]
 
 
 _cuda = None

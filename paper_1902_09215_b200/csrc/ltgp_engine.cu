@@ -162,7 +162,8 @@ struct Slice {
     uint64_t src, dst, len;
 };
 constexpr uint32_t kMaxSlices = 64;
-constexpr int kComputeStreams = 4;     // slice g runs on compute stream g % 4
+constexpr int kComputeStreams = 4;
+constexpr uint32_t kCpopsSmem = 96 * 1024;  // k_cpops's shared segment stack (2 per chunk of a tree)     // slice g runs on compute stream g % 4
 constexpr uint64_t kSlicePad = 2048;   // arena gap between slices (k_eval's record look-ahead < 1 KB)
 // target bytes per slice, slice count cap (LTGP_SLICE_MB / LTGP_SLICES override)
 uint64_t slice_bytes() {
@@ -198,14 +199,16 @@ struct Shard {
     TreeSet scratch;                // ltgp_eval_one
     // evaluation scratch
     DevBuf items, ctrees, hdr, steps, frames, dframes, segs, spill, counters, rec, outs;
+    DevBuf runs, cch, cres, saddr, big_addr[2];  // spine combine: pop runs, per chunk / tree, step operand addresses
     DevBuf big_steps[2], big_frames[2], rerun_items[2], rerun_slot[2], ovf, big_spill;  // overflow re-runs (2 tiers)
     double rerun_ksecs = 0.0, rerun_csecs = 0.0;
     bool last_outs = false;
     uint32_t last_reruns = 0;
     HostBuf h_items, h_ctrees, h_counters;
-    uint32_t last_items = 0, last_chunks = 0, last_ctrees = 0;
+    uint32_t last_items = 0, last_chunks = 0, last_ctrees = 0, max_tree_chunks = 0;
     uint32_t cur_chunk = kDefaultChunk, cur_max_frames = kMaxFrames, cur_max_steps = kMaxSteps;
     double pool_per_chunk_f = 0.0, pool_per_chunk_s = 0.0;  // summary pool claimed per chunk (last evaluation)
+    uint64_t last_steps = 0;                                  // spine steps claimed (last evaluation)
     EvalArgs eargs;      // arguments of the last evaluation (for overflow reruns)
     CombineArgs cargs;
     const TreeSet* items_for = nullptr;  // work list cache: (set, version)
@@ -220,7 +223,8 @@ struct Shard {
         for (DevBuf* b : {&items, &ctrees, &hdr, &steps, &frames, &dframes, &segs, &spill, &counters,
                           &rec, &outs, &plans, &ext, &csize, &coff, &dir, &big_steps[0], &big_frames[0],
                           &big_steps[1], &big_frames[1], &rerun_items[0], &rerun_slot[0], &rerun_items[1],
-                          &rerun_slot[1], &ovf, &big_spill, &gstats}) b->release();
+                          &rerun_slot[1], &ovf, &big_spill, &gstats, &runs, &cch, &cres, &saddr, &big_addr[0],
+                          &big_addr[1]}) b->release();
         h_gstats.release();
         h_items.release(); h_ctrees.release(); h_counters.release();
         h_csize.release(); h_coff.release(); h_dir.release();
@@ -287,6 +291,7 @@ int init_shard(ltgp_engine* e, Shard& s) {
     s.sms = prop.multiProcessorCount;
     const size_t smem = eval_smem_bytes();
     CK(cudaFuncSetAttribute(K_EVAL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k_cpops, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCpopsSmem));
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K_EVAL, kWarps * 32, smem));
     if (per_sm < 1) { set_err("k_eval does not fit on an SM"); return -1; }
@@ -296,6 +301,8 @@ int init_shard(ltgp_engine* e, Shard& s) {
     TRY(s.h_counters.ensure(64));
     return 0;
 }
+
+int launch_combine(ltgp_engine* e, Shard& s, uint32_t& launches);
 
 // Evaluate every tree of `ts` on shard s: records (and optional per-case
 // outputs) land in rec/outs. Asynchronous on s.st.
@@ -351,7 +358,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         std::vector<Item> all;
         std::vector<CombineTree> ctrees;
         s.slice_items.assign(G + 1, 0);
-        uint32_t nch = 0;
+        uint32_t nch = 0, max_chunks = 0;
         all.reserve(ts.count + 64);
         for (uint32_t g = 0; g < G; ++g) {
             s.slice_items[g] = (uint32_t)all.size();
@@ -366,6 +373,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
                 }
                 const uint32_t k = (n + C - 1) / C;
                 ctrees.push_back({t, nch, k, n});
+                max_chunks = std::max(max_chunks, k);
                 for (uint32_t j = 0; j < k; ++j) all.push_back({t, nch + j, j * C, std::min(n, (j + 1) * C)});
                 nch += k;
             }
@@ -400,10 +408,14 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             TRY(s.hdr.ensure(sizeof(ChunkHdr) * nch, s.dev));
             TRY(s.dframes.ensure((size_t)kFrameBytes * nch, s.dev));
             TRY(s.segs.ensure(sizeof(Seg) * 2 * nch, s.dev));
+            TRY(s.runs.ensure(sizeof(PopRun) * 3 * nch, s.dev));
+            TRY(s.cch.ensure(sizeof(CombChunk) * nch, s.dev));
+            TRY(s.cres.ensure(sizeof(CombResult) * nct, s.dev));
         }
         s.last_items = nitems;
         s.last_chunks = nch;
         s.last_ctrees = nct;
+        s.max_tree_chunks = max_chunks;
         s.items_for = &ts;
         s.items_version = ts.version;
         s.items_slices = tb;
@@ -426,6 +438,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         pool.frames = s.frames.as<float2>();
         pool.steps = s.steps.as<uint8_t>();
         pool.used = reinterpret_cast<unsigned long long*>(s.counters.as<uint32_t>() + kPoolCounters);
+        TRY(s.saddr.ensure((size_t)pool.cap_steps * 8, s.dev));
     }
     pool.spill_frames = spill_frames(s.cur_chunk);
     pool.adjusts = s.counters.as<uint32_t>() + 5;  // inline window adjusts join the statistics
@@ -458,8 +471,14 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     ca.trees = s.ctrees.as<CombineTree>();
     ca.n_trees = nct;
     ca.hdr = s.hdr.as<ChunkHdr>();
+    ca.n_chunks = nch;
     ca.dframes = s.dframes.as<float2>();
     ca.segs = s.segs.as<Seg>();
+    ca.runs = s.runs.as<PopRun>();
+    ca.cch = s.cch.as<CombChunk>();
+    ca.cres = s.cres.as<CombResult>();
+    ca.space[0] = StepSpace{s.steps.as<uint8_t>(), nch ? pool.cap_steps : 0, s.saddr.as<uint64_t>()};
+    ca.space[1] = ca.space[2] = StepSpace{nullptr, 0, nullptr};
     ca.rec = s.rec.as<float>();
     ca.outs = a.outs;
     ca.counters = s.counters.as<uint32_t>();
@@ -544,13 +563,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         for (uint32_t g = G > (uint32_t)kComputeStreams ? G - kComputeStreams : 0; g < G; ++g)
             if (g % kComputeStreams) CK(cudaStreamWaitEvent(s.st, s.sev[3 * g + 2], 0));
     CK(cudaEventRecord(s.ev[4], s.st));
-    if (nct) {
-        const int blocks = (int)std::min<uint32_t>((nct + kCombineWarps - 1) / kCombineWarps, (uint32_t)s.sms * 16);
-        k_combine<<<blocks, kCombineWarps * 32, 0, s.st>>>(ca, e->suite);
-        CK(cudaGetLastError());
-        DEBUG_SYNC(s.st, "k_combine");
-        ++launches;
-    }
+    if (nct) TRY(launch_combine(e, s, launches));
     CK(cudaEventRecord(s.ev[1], s.st));
     CK(cudaMemcpyAsync(s.h_counters.p, s.counters.p, 64, cudaMemcpyDeviceToHost, s.st));
     e->stats.kernel_launches = launches;
@@ -565,6 +578,27 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
 // on a small grid with its own spill area; then every chunked tree is
 // recombined once. Synchronous; only taken when the counters report an
 // overflow. Device time is added to the evaluation's.
+// The spine combine of the chunked trees (k_cpops -> k_caddr -> k_combine)
+// on s.st, with s.cargs.
+int launch_combine(ltgp_engine* e, Shard& s, uint32_t& launches) {
+    const CombineArgs& ca = s.cargs;
+    // k_cpops's segment stack in shared memory: 2 per chunk of the tree
+    const uint32_t segs = std::min<uint32_t>(2 * s.max_tree_chunks, kCpopsSmem / (uint32_t)sizeof(Seg));
+    k_cpops<<<ca.n_trees, 32, segs * sizeof(Seg), s.st>>>(ca, segs);
+    CK(cudaGetLastError());
+    DEBUG_SYNC(s.st, "k_cpops");
+    const uint32_t ablocks = std::min<uint32_t>((ca.n_chunks + 3) / 4, (uint32_t)s.sms * 16);
+    k_caddr<<<std::max<uint32_t>(ablocks, 1), 128, 0, s.st>>>(ca);
+    CK(cudaGetLastError());
+    DEBUG_SYNC(s.st, "k_caddr");
+    const int blocks = (int)std::min<uint32_t>((ca.n_trees + kCombineWarps - 1) / kCombineWarps, (uint32_t)s.sms * 16);
+    k_combine<<<blocks, kCombineWarps * 32, 0, s.st>>>(ca, e->suite);
+    CK(cudaGetLastError());
+    DEBUG_SYNC(s.st, "k_combine");
+    launches += 3;
+    return 0;
+}
+
 int rerun_overflowed(ltgp_engine* e, Shard& s) {
     CK(cudaSetDevice(s.dev));
     const uint32_t C = s.cur_chunk;
@@ -597,6 +631,8 @@ int rerun_overflowed(ltgp_engine* e, Shard& s) {
         DevBuf& bframes = s.big_frames[tier - 1];
         TRY(bsteps.ensure((size_t)n * scap, s.dev));
         TRY(bframes.ensure((size_t)n * fcap * kFrameBytes, s.dev));
+        TRY(s.big_addr[tier - 1].ensure((size_t)n * scap * 8, s.dev));
+        s.cargs.space[tier] = StepSpace{bsteps.as<uint8_t>(), (uint64_t)n * scap, s.big_addr[tier - 1].as<uint64_t>()};
         int grid;
         EvalArgs a = s.eargs;
         if (worst) {
@@ -638,15 +674,14 @@ int rerun_overflowed(ltgp_engine* e, Shard& s) {
     }
     if (s.last_ctrees) {
         CK(cudaEventRecord(s.ev[5], s.st));
-        const int blocks = (int)std::min<uint32_t>((s.last_ctrees + kCombineWarps - 1) / kCombineWarps, (uint32_t)s.sms * 16);
-        k_combine<<<blocks, kCombineWarps * 32, 0, s.st>>>(s.cargs, e->suite);
-        CK(cudaGetLastError());
+        uint32_t nl = 0;
+        TRY(launch_combine(e, s, nl));
         CK(cudaEventRecord(s.ev[6], s.st));
         CK(cudaMemcpyAsync(s.h_counters.p, s.counters.p, 64, cudaMemcpyDeviceToHost, s.st));
         CK(cudaStreamSynchronize(s.st));
         CK(cudaEventElapsedTime(&ms, s.ev[5], s.ev[6]));
         s.rerun_csecs += ms * 1e-3;
-        e->stats.kernel_launches += 1;
+        e->stats.kernel_launches += nl;
     }
     hc[1] |= keep;
     hc[4] = exits;
@@ -671,12 +706,14 @@ int check_eval(Shard& s) {
 // After the stream is synchronized: re-run overflowed chunks if any.
 int finish_eval(ltgp_engine* e, Shard& s) {
     const uint32_t* c = s.h_counters.as<uint32_t>();
+    s.last_steps = 0;
     if (s.last_chunks) {  // what this evaluation's chunks claimed from the summary pool
         uint64_t uf, us;
         std::memcpy(&uf, c + kPoolCounters, 8);
         std::memcpy(&us, c + kPoolCounters + 2, 8);
         s.pool_per_chunk_f = (double)uf / s.last_chunks;
         s.pool_per_chunk_s = (double)us / s.last_chunks;
+        s.last_steps = us;
     }
     if (c[2] != 0) TRY(rerun_overflowed(e, s));
     return check_eval(s);
@@ -737,7 +774,7 @@ int upload_tables(Shard& s, TreeSet& ts) {
 
 int collect(ltgp_engine* e, ltgp_record* out, float* outs48) {
     double secs = 0.0, ksecs = 0.0, csecs = 0.0;
-    uint64_t nodes = 0, chunks = 0, reruns = 0, exits = 0, adjusts = 0;
+    uint64_t nodes = 0, chunks = 0, reruns = 0, exits = 0, adjusts = 0, steps = 0;
     for (Shard& s : e->shards) {
         if (!s.count) continue;
         CK(cudaSetDevice(s.dev));
@@ -764,7 +801,9 @@ int collect(ltgp_engine* e, ltgp_record* out, float* outs48) {
         reruns += s.last_reruns;
         exits += s.h_counters.as<uint32_t>()[4];
         adjusts += s.h_counters.as<uint32_t>()[5];
+        steps += s.last_steps;
     }
+    e->stats.last_spine_steps = steps;
     e->stats.last_exits = exits;
     e->stats.last_window_adjusts = adjusts;
     e->stats.last_fallback_items = reruns;

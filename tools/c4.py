@@ -38,7 +38,7 @@ def main():
             print(f"eval {st['eval_seconds']*1e3:.1f} ms (k_eval {st['eval_kernel_seconds']*1e3:.1f}, combine "
                   f"{st['combine_seconds']*1e3:.1f}) {tot*48/st['eval_seconds']/1e12:.3f} T GPops/s, chunks "
                   f"{st['last_chunks']}, reruns {st['last_fallback_items']}, exits {st['last_exits']}, "
-                  f"adjusts {st['last_window_adjusts']}", flush=True)
+                  f"adjusts {st['last_window_adjusts']}, spine steps {st['last_spine_steps']}", flush=True)
     if a.cpu_trees:  # the reference's CPU path (oracle port), one tree per thread as the reference does
         from tests._oracle import load_oracle
         o = load_oracle()
