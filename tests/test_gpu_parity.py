@@ -117,6 +117,14 @@ def test_remy_deep_trees(oracle, suite, chunk):
     check_population(oracle, suite, genomes, chunk=chunk)
 
 
+def test_combine_many_chunks(oracle, suite):
+    """Trees of more chunks than k_cpops's shared-memory segment stack holds
+    (over 3072 chunks: its stack falls back to global memory) next to
+    smaller chunked trees in the same launch."""
+    genomes = [ltgp.remy_tree(90, 400001), ltgp.remy_tree(91, 5001), ltgp.random_tree_of_size(92, 250001)]
+    check_population(oracle, suite, genomes, chunk=64)
+
+
 def test_adversarial(oracle, suite):
     c0 = 5 + int(np.argmin(np.abs(suite[2])))  # constant nearest 0 (may be 0.000)
     gs = []
