@@ -346,6 +346,28 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             while (C < kDefaultChunk && (uint64_t)C * 2 <= per) C *= 2;
             const double want = std::pow(1.25 * (double)biggest, 2.0 / 3.0);
             while (C < kMaxChunk && (double)C < want) C *= 2;
+            // Wave balance: when chunks fill only a few waves of the
+            // persistent grid, the last wave runs part-full (48 x 1e7 nodes
+            // at 65536: 7344 chunks on 4736 warps, 2 waves at 77%). Shorten
+            // the chunks (down to C/2, multiples of 1024) to the shortest
+            // length that keeps the same number of waves.
+            const uint64_t W = (uint64_t)s.eval_grid * kWarps;
+            auto chunks_of = [&](uint32_t c) {
+                uint64_t k = 0;
+                for (uint32_t t = 0; t < ts.count; ++t)
+                    if (ts.h_size[t] > c) k += (ts.h_size[t] + c - 1) / c;
+                return k;
+            };
+            const uint64_t k0 = chunks_of(C);
+            const uint64_t waves = (k0 + W - 1) / W;
+            if (k0 > W / 2 && waves <= 8 && C >= 2048) {
+                uint32_t lo = std::max<uint32_t>(1024, C / 2) / 1024, hi = C / 1024;  // in units of 1024
+                while (lo < hi) {  // smallest c with chunks_of(c) <= waves * W (non-increasing in c)
+                    const uint32_t mid = (lo + hi) / 2;
+                    if (chunks_of(mid * 1024) <= waves * W) hi = mid; else lo = mid + 1;
+                }
+                C = hi * 1024;
+            }
         }
         // chunk summaries are sized exactly by k_plan (PlanPool); these are
         // the per-chunk capacities of the first overflow re-run tier (x4).
