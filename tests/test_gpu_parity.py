@@ -125,6 +125,30 @@ def test_combine_many_chunks(oracle, suite):
     check_population(oracle, suite, genomes, chunk=64)
 
 
+def test_auto_chunk_wave_balance(oracle, suite):
+    """Automatic chunk length with the wave balance: 100 trees of 3e5 nodes
+    get 8192-node chunks from the power-of-two rule (3700 chunks, one part-
+    full wave of the persistent grid), shortened to the shortest multiple of
+    1024 that keeps one wave -- a length that is not a power of two."""
+    import torch
+    n, T = 300001, 100
+    genomes = [ltgp.random_tree_of_size(500 + k, n) for k in range(T)]
+    W = torch.cuda.get_device_properties(0).multi_processor_count * 32
+    chunks = lambda c: T * -(-n // c)
+    waves = -(-chunks(8192) // W)
+    c = next(c for c in range(4096, 8193, 1024) if chunks(c) <= waves * W)
+    with engine(suite) as e:
+        e.upload_population(genomes)
+        rec, outs = e.evaluate_outputs()
+        assert e.stats()["last_chunks"] == chunks(c)
+    assert c % 1024 == 0 and c & (c - 1)  # not a power of two on a 148-SM B200
+    buf, offs, sizes = pack(genomes)
+    assert_records_equal(rec, oracle.evaluate_population(buf, offs, sizes, suite, threads=0))
+    for k in (0, T - 1):
+        o, _ = oracle.eval_batch(genomes[k], suite[0], suite[2])
+        assert same_bits(outs[k], o)
+
+
 def test_adversarial(oracle, suite):
     c0 = 5 + int(np.argmin(np.abs(suite[2])))  # constant nearest 0 (may be 0.000)
     gs = []

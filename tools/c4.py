@@ -19,6 +19,8 @@ def main():
     ap.add_argument("--check", type=int, default=2)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--chunk", type=int, default=0)
+    ap.add_argument("--ops", default="",
+                    help="remap function opcodes (e.g. '0120': division -> add) to study the op mix")
     ap.add_argument("--cpu-trees", type=int, default=0,
                     help="time the CPU oracle (evaluate_population, all host threads) on this many trees")
     a = ap.parse_args()
@@ -27,6 +29,10 @@ def main():
     with ThreadPoolExecutor(os.cpu_count()) as ex:
         trees = list(ex.map(lambda i: ltgp.remy_tree(7000 + i, n), range(a.trees)))
     print(f"generated {a.trees} x {n} nodes in {time.perf_counter() - t:.1f} s", flush=True)
+    if a.ops:  # opcodes 0..3 -> the given ones (leaves unchanged)
+        lut = np.arange(256, dtype=np.uint8)
+        lut[:4] = [int(c) for c in a.ops]
+        trees = [lut[g] for g in trees]
     suite = ltgp.make_suite(ltgp.suite_seed(1))
     with ltgp.Engine([0], node_limit=2**62, chunk_nodes=a.chunk) as e:
         e.set_suite(*suite)
