@@ -162,22 +162,30 @@ struct Slice {
     uint64_t src, dst, len;
 };
 constexpr uint32_t kMaxSlices = 64;
-constexpr int kComputeStreams = 4;
-constexpr uint32_t kCpopsSmem = 96 * 1024;  // k_cpops's shared segment stack (2 per chunk of a tree)     // slice g runs on compute stream g % 4
+constexpr int kComputeStreams = 4;     // slice g runs on compute stream g % 4
+constexpr uint32_t kCpopsSmem = 96 * 1024;  // k_cpops's shared segment stack (2 per chunk of a tree)
 constexpr uint64_t kSlicePad = 2048;   // arena gap between slices (k_eval's record look-ahead < 1 KB)
-// target bytes per slice, slice count cap (LTGP_SLICE_MB / LTGP_SLICES override)
-uint64_t slice_bytes() {
-    static const uint64_t v = std::getenv("LTGP_SLICE_MB") ? std::atoll(std::getenv("LTGP_SLICE_MB")) << 20 : 32ull << 20;
+// LTGP_TRACE=1: a streamed evaluation prints when each slice's copy, plan
+// and evaluation ended (ms after the call's first event), to stderr
+bool trace_slices() {
+    static const bool v = std::getenv("LTGP_TRACE") != nullptr;
     return v;
 }
+
+// target bytes per slice and slice count cap of a streamed evaluation
+// (LTGP_SLICE_KB / LTGP_SLICES override them; read per call)
+uint64_t slice_bytes() {
+    const char* v = std::getenv("LTGP_SLICE_KB");
+    return v ? std::max<uint64_t>(1, std::strtoull(v, nullptr, 10)) << 10 : 16ull << 20;
+}
 uint32_t max_slices() {
-    static const uint32_t v = std::getenv("LTGP_SLICES") ? std::min<uint32_t>(kMaxSlices, std::atoi(std::getenv("LTGP_SLICES")))
-                                                         : 16u;
-    return v;
+    const char* v = std::getenv("LTGP_SLICES");
+    return v ? (uint32_t)std::min<long>(kMaxSlices, std::max<long>(1, std::strtol(v, nullptr, 10))) : 24u;
 }
 constexpr uint32_t kQueueBase = 16;    // counters[16 + g]: work queue of slice g
 constexpr uint32_t kPoolCounters = 8;  // counters[8..11]: chunk-summary pool claims (2 x u64)
-constexpr size_t kCounterBytes = 256;
+constexpr size_t kCounterBytes = 512;
+static_assert(kCounterBytes >= 4 * (kQueueBase + kMaxSlices), "every slice needs its queue counter");
 
 struct Shard {
     int dev = 0;
@@ -188,6 +196,7 @@ struct Shard {
     std::vector<Slice> slices;                  // non-empty during a streamed evaluation
     const uint8_t* src = nullptr;               // its pinned host source
     std::vector<uint32_t> slice_items;          // slice g's items: [slice_items[g], slice_items[g+1])
+    std::vector<uint32_t> slice_ct, slice_ch;   // slice g's chunked trees / chunks (same convention)
     std::vector<uint32_t> items_slices;         // work-list cache key (slice tree boundaries)
     DevBuf xspill[kComputeStreams];             // spill areas of xs[1..] (xs[0] uses spill)
     cudaEvent_t ev[8] = {};
@@ -280,7 +289,7 @@ int init_shard(ltgp_engine* e, Shard& s) {
     CK(cudaStreamCreateWithFlags(&s.cst, cudaStreamNonBlocking));
     for (auto& ev : s.ev) CK(cudaEventCreate(&ev));
     s.sev.resize(3 * kMaxSlices);
-    for (auto& ev : s.sev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    for (auto& ev : s.sev) CK(cudaEventCreateWithFlags(&ev, trace_slices() ? cudaEventDefault : cudaEventDisableTiming));
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, s.dev));
     if (prop.major < 10) {
@@ -302,7 +311,7 @@ int init_shard(ltgp_engine* e, Shard& s) {
     return 0;
 }
 
-int launch_combine(ltgp_engine* e, Shard& s, uint32_t& launches);
+int launch_combine(ltgp_engine* e, Shard& s, const CombineArgs& ca, cudaStream_t st, uint32_t& launches);
 
 // Evaluate every tree of `ts` on shard s: records (and optional per-case
 // outputs) land in rec/outs. Asynchronous on s.st.
@@ -380,23 +389,31 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         std::vector<Item> all;
         std::vector<CombineTree> ctrees;
         s.slice_items.assign(G + 1, 0);
+        s.slice_ct.assign(G + 1, 0);
+        s.slice_ch.assign(G + 1, 0);
         uint32_t nch = 0, max_chunks = 0;
         all.reserve(ts.count + 64);
         for (uint32_t g = 0; g < G; ++g) {
             s.slice_items[g] = (uint32_t)all.size();
+            s.slice_ct[g] = (uint32_t)ctrees.size();
+            s.slice_ch[g] = nch;
+            // the last slice of a streamed evaluation is all that runs after
+            // the final copy: shorter chunks shorten that tail (an item's
+            // latency is ~C / 13e6 s)
+            const uint32_t Cg = (G > 1 && g == G - 1) ? std::max<uint32_t>(1024, C / 4) : C;
             // whole trees largest first for load balance: by log2(size)
             // buckets, descending (linear; stable within a bucket)
             uint32_t bcount[33] = {};
             for (uint32_t t = tb[g]; t < tb[g + 1]; ++t) {
                 const uint32_t n = ts.h_size[t];
-                if (n <= C) {
+                if (n <= Cg) {
                     ++bcount[32 - __builtin_clz(n)];
                     continue;
                 }
-                const uint32_t k = (n + C - 1) / C;
+                const uint32_t k = (n + Cg - 1) / Cg;
                 ctrees.push_back({t, nch, k, n});
                 max_chunks = std::max(max_chunks, k);
-                for (uint32_t j = 0; j < k; ++j) all.push_back({t, nch + j, j * C, std::min(n, (j + 1) * C)});
+                for (uint32_t j = 0; j < k; ++j) all.push_back({t, nch + j, j * Cg, std::min(n, (j + 1) * Cg)});
                 nch += k;
             }
             uint32_t bstart[33];
@@ -408,10 +425,12 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             all.resize(pos);
             for (uint32_t t = tb[g]; t < tb[g + 1]; ++t) {
                 const uint32_t n = ts.h_size[t];
-                if (n <= C) all[bstart[32 - __builtin_clz(n)]++] = Item{t, kWholeTree, 0, n};
+                if (n <= Cg) all[bstart[32 - __builtin_clz(n)]++] = Item{t, kWholeTree, 0, n};
             }
         }
         s.slice_items[G] = (uint32_t)all.size();
+        s.slice_ct[G] = (uint32_t)ctrees.size();
+        s.slice_ch[G] = nch;
         const uint32_t nitems = (uint32_t)all.size();
         // the pinned staging buffers are reused: wait for their last copies
         // (not for the whole stream: a splice may still be running)
@@ -494,6 +513,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     ca.n_trees = nct;
     ca.hdr = s.hdr.as<ChunkHdr>();
     ca.n_chunks = nch;
+    ca.chunk0 = 0;
     ca.dframes = s.dframes.as<float2>();
     ca.segs = s.segs.as<Seg>();
     ca.runs = s.runs.as<PopRun>();
@@ -579,13 +599,24 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             DEBUG_SYNC(X, "k_eval");
             ++launches;
         }
+        if (streamed && s.slice_ct[g + 1] > s.slice_ct[g]) {
+            // this slice's chunked trees, combined on its stream right away
+            // (only the last slice's combine is left after the final copy)
+            CombineArgs cg = ca;
+            cg.trees = ca.trees + s.slice_ct[g];
+            cg.cres = ca.cres + s.slice_ct[g];
+            cg.n_trees = s.slice_ct[g + 1] - s.slice_ct[g];
+            cg.chunk0 = s.slice_ch[g];
+            cg.n_chunks = s.slice_ch[g + 1] - s.slice_ch[g];
+            TRY(launch_combine(e, s, cg, X, launches));
+        }
         if (streamed) CK(cudaEventRecord(s.sev[3 * g + 2], X));
     }
     if (streamed)  // join the other compute streams: the last slice each ran
         for (uint32_t g = G > (uint32_t)kComputeStreams ? G - kComputeStreams : 0; g < G; ++g)
             if (g % kComputeStreams) CK(cudaStreamWaitEvent(s.st, s.sev[3 * g + 2], 0));
     CK(cudaEventRecord(s.ev[4], s.st));
-    if (nct) TRY(launch_combine(e, s, launches));
+    if (nct && !streamed) TRY(launch_combine(e, s, ca, s.st, launches));
     CK(cudaEventRecord(s.ev[1], s.st));
     CK(cudaMemcpyAsync(s.h_counters.p, s.counters.p, 64, cudaMemcpyDeviceToHost, s.st));
     e->stats.kernel_launches = launches;
@@ -600,23 +631,23 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
 // on a small grid with its own spill area; then every chunked tree is
 // recombined once. Synchronous; only taken when the counters report an
 // overflow. Device time is added to the evaluation's.
-// The spine combine of the chunked trees (k_cpops -> k_caddr -> k_combine)
-// on s.st, with s.cargs.
-int launch_combine(ltgp_engine* e, Shard& s, uint32_t& launches) {
-    const CombineArgs& ca = s.cargs;
+// The spine combine (k_cpops -> k_caddr -> k_combine) of the chunked trees
+// and chunks `ca` names, on stream st.
+int launch_combine(ltgp_engine* e, Shard& s, const CombineArgs& ca, cudaStream_t st, uint32_t& launches) {
+    if (ca.n_trees == 0) return 0;
     // k_cpops's segment stack in shared memory: 2 per chunk of the tree
     const uint32_t segs = std::min<uint32_t>(2 * s.max_tree_chunks, kCpopsSmem / (uint32_t)sizeof(Seg));
-    k_cpops<<<ca.n_trees, 32, segs * sizeof(Seg), s.st>>>(ca, segs);
+    k_cpops<<<ca.n_trees, 32, segs * sizeof(Seg), st>>>(ca, segs);
     CK(cudaGetLastError());
-    DEBUG_SYNC(s.st, "k_cpops");
+    DEBUG_SYNC(st, "k_cpops");
     const uint32_t ablocks = std::min<uint32_t>((ca.n_chunks + 3) / 4, (uint32_t)s.sms * 16);
-    k_caddr<<<std::max<uint32_t>(ablocks, 1), 128, 0, s.st>>>(ca);
+    k_caddr<<<std::max<uint32_t>(ablocks, 1), 128, 0, st>>>(ca);
     CK(cudaGetLastError());
-    DEBUG_SYNC(s.st, "k_caddr");
+    DEBUG_SYNC(st, "k_caddr");
     const int blocks = (int)std::min<uint32_t>((ca.n_trees + kCombineWarps - 1) / kCombineWarps, (uint32_t)s.sms * 16);
-    k_combine<<<blocks, kCombineWarps * 32, 0, s.st>>>(ca, e->suite);
+    k_combine<<<blocks, kCombineWarps * 32, 0, st>>>(ca, e->suite);
     CK(cudaGetLastError());
-    DEBUG_SYNC(s.st, "k_combine");
+    DEBUG_SYNC(st, "k_combine");
     launches += 3;
     return 0;
 }
@@ -697,7 +728,7 @@ int rerun_overflowed(ltgp_engine* e, Shard& s) {
     if (s.last_ctrees) {
         CK(cudaEventRecord(s.ev[5], s.st));
         uint32_t nl = 0;
-        TRY(launch_combine(e, s, nl));
+        TRY(launch_combine(e, s, s.cargs, s.st, nl));
         CK(cudaEventRecord(s.ev[6], s.st));
         CK(cudaMemcpyAsync(s.h_counters.p, s.counters.p, 64, cudaMemcpyDeviceToHost, s.st));
         CK(cudaStreamSynchronize(s.st));
@@ -1095,10 +1126,17 @@ int ltgp_evaluate_packed(ltgp_engine* e, uint32_t M, const uint8_t* buf, uint64_
         const uint64_t span = end - base;
         const uint32_t G = (uint32_t)std::min<uint64_t>(max_slices(), std::max<uint64_t>(1, span / slice_bytes()));
         s.slices.clear();
+        // the last three slices taper (1/2, 1/4, 1/8 of the others): what is
+        // left to evaluate after the final copy is short
+        auto weight = [&](uint32_t g) -> uint64_t { return G >= 4 && g + 3 >= G ? 8u >> (g + 4 - G) : 8u; };
+        uint64_t wsum = 0;
+        for (uint32_t g = 0; g < G; ++g) wsum += weight(g);
+        uint64_t wcum = 0;
         uint32_t t = 0;
         uint64_t dst = 0;
         for (uint32_t g = 0; g < G && t < s.count; ++g) {
-            const uint64_t goal = base + span * (g + 1) / G;
+            wcum += weight(g);
+            const uint64_t goal = base + span * wcum / wsum;
             const uint32_t t0 = t;
             do { ++t; } while (t < s.count && (g == G - 1 || offsets[s.first + t] < goal));
             const uint64_t src = offsets[s.first + t0];
@@ -1113,6 +1151,19 @@ int ltgp_evaluate_packed(ltgp_engine* e, uint32_t M, const uint8_t* buf, uint64_
         TRY(upload_tables(s, ts));
         s.src = buf;
         const int rc = launch_eval(e, s, ts, outs48 != nullptr);
+        if (rc == 0 && trace_slices()) {
+            CK(cudaStreamSynchronize(s.st));
+            float t[3], tot = 0.0f;
+            CK(cudaEventElapsedTime(&tot, s.ev[0], s.ev[1]));
+            std::fprintf(stderr, "ltgp trace: %zu slices, %.3f ms to the last record\n", s.slices.size(), tot);
+            for (size_t g = 0; g < s.slices.size(); ++g) {
+                for (int k = 0; k < 3; ++k) CK(cudaEventElapsedTime(&t[k], s.ev[0], s.sev[3 * g + k]));
+                std::fprintf(stderr, "  slice %2zu: %7.2f MB, %3u trees, copied %7.3f planned %7.3f evaluated %7.3f\n", g,
+                             s.slices[g].len / 1e6,
+                             (g + 1 < s.slices.size() ? s.slices[g + 1].tree_begin : s.count) - s.slices[g].tree_begin,
+                             t[0], t[1], t[2]);
+            }
+        }
         s.slices.clear();
         s.src = nullptr;
         TRY(rc);

@@ -391,6 +391,27 @@ def test_streamed_small_and_outputs(oracle, suite):
         assert same_bits(outs[k], o)
 
 
+def test_streamed_slice_cap(oracle, suite, monkeypatch):
+    """The streamed path at its slice-count cap (64 slices of ~9 KB, every
+    slice with its own work queue), record- and output-identical to the
+    oracle; then the defaults again on the same engine."""
+    buf, offs, sizes = ltgp.corpus(31, 600, 2.0, 3.5)
+    exp = oracle.evaluate_population(buf, offs, sizes, suite, threads=0)
+    with engine(suite, chunk=1024) as e:
+        monkeypatch.setenv("LTGP_SLICES", "64")
+        monkeypatch.setenv("LTGP_SLICE_KB", "8")
+        rec, outs = e.evaluate_packed(buf, offs, sizes, outputs=True)
+        assert_records_equal(rec, exp)
+        for k in (0, 299, 599):
+            g = buf[int(offs[k]):int(offs[k]) + int(sizes[k])]
+            o, _ = oracle.eval_batch(g, suite[0], suite[2])
+            assert same_bits(outs[k], o)
+        monkeypatch.delenv("LTGP_SLICES")
+        monkeypatch.delenv("LTGP_SLICE_KB")
+        rec = e.evaluate_packed(buf, offs, sizes)
+        assert_records_equal(rec, exp)
+
+
 @pytest.mark.slow
 def test_config2_bloating_run_matches_oracle(oracle, tmp_path):
     """Config 2 scale: pop 4000, tournament 7, no size limit, 100 generations
