@@ -61,6 +61,21 @@ int64_t ltgp_host_run(ltgp_engine* e, uint32_t M, uint32_t max_generations, uint
                       uint32_t k, uint64_t seed, int grow_mode, uint64_t memory_budget,
                       const char* dump_path, int* reason, uint64_t* nodes_evaluated, double* eval_seconds);
 
+/* ltgp_host_run with checkpoint/resume: when
+   ckpt_every > 0, after generation 0 and every ckpt_every-th generation (and
+   the last) the population's genomes (downloaded from the device), records,
+   Rng stream position and run counters are written to ckpt_path (atomically,
+   via ckpt_path.tmp). resume_path (NULL: fresh start) continues a run from
+   such a file: the parameters must equal the checkpointed run's (else error),
+   the parents are re-uploaded with their records restored, the dump is
+   appended to, and the return value and *nodes_evaluated / *eval_seconds
+   count the whole run. A resumed run's dump equals the uninterrupted run's. */
+int64_t ltgp_host_run_checkpointed(ltgp_engine* e, uint32_t M, uint32_t max_generations, uint64_t node_limit,
+                                   uint32_t k, uint64_t seed, int grow_mode, uint64_t memory_budget,
+                                   const char* dump_path, const char* ckpt_path, uint32_t ckpt_every,
+                                   const char* resume_path, int* reason, uint64_t* nodes_evaluated,
+                                   double* eval_seconds);
+
 #ifdef __cplusplus
 }
 #endif

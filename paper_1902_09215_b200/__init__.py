@@ -100,6 +100,10 @@ _HOST_SIGS = {
     "ltgp_host_run": (C.c_int64, [_P, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint64, C.c_int, C.c_uint64,
                                   C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_uint64),
                                   C.POINTER(C.c_double)]),
+    "ltgp_host_run_checkpointed": (C.c_int64, [_P, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint64,
+                                               C.c_int, C.c_uint64, C.c_char_p, C.c_char_p, C.c_uint32,
+                                               C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_uint64),
+                                               C.POINTER(C.c_double)]),
 }
 
 
@@ -386,15 +390,20 @@ class Engine:
         return p.value, f.value, n.value, st.value
 
     def run(self, M: int, generations: int, node_limit: int, k: int = 7, seed: int = 1,
-            dump_path: str | None = None, grow_mode: int = 0, memory_budget: int = 0):
+            dump_path: str | None = None, grow_mode: int = 0, memory_budget: int = 0,
+            checkpoint: str | None = None, checkpoint_every: int = 0, resume: str | None = None):
         """run() (run.hpp:33-36) driven from C++ on this engine; reason 0
-        MaxGenerations, 1 SizeLimitHit, 2 MemoryBudgetExceeded."""
+        MaxGenerations, 1 SizeLimitHit, 2 MemoryBudgetExceeded. With
+        checkpoint_every > 0 the run state is written to `checkpoint` every
+        that many generations; `resume` continues from such a file."""
         reason = C.c_int()
         nodes = C.c_uint64()
         secs = C.c_double()
-        done = host_lib().ltgp_host_run(self._h, M, generations, node_limit, k, seed, grow_mode, memory_budget,
-                                        dump_path.encode() if dump_path else None,
-                                        C.byref(reason), C.byref(nodes), C.byref(secs))
+        enc = lambda p: p.encode() if p else None  # noqa: E731
+        done = host_lib().ltgp_host_run_checkpointed(self._h, M, generations, node_limit, k, seed, grow_mode,
+                                                     memory_budget, enc(dump_path), enc(checkpoint),
+                                                     checkpoint_every, enc(resume),
+                                                     C.byref(reason), C.byref(nodes), C.byref(secs))
         if done < 0:
             raise EngineError(_err() or "ltgp_host_run failed")
         return {"generations": int(done), "reason": int(reason.value), "nodes": int(nodes.value),

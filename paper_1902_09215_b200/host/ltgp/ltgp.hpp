@@ -18,7 +18,9 @@
 #include <limits>
 #include <random>
 #include <span>
+#include <sstream>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 #include "../../../include/ltgp_cuda.h"
@@ -63,6 +65,18 @@ public:
         return static_cast<float>(2.0 * u - 1.0);
     }
     std::uint64_t draw_count() const { return draws_; }
+    // Checkpoint/resume: the engine state in the
+    // standard's portable text form, then the draw counter.
+    std::string state() const {
+        std::ostringstream os;
+        os << engine_ << ' ' << draws_;
+        return os.str();
+    }
+    void set_state(const std::string& s) {
+        std::istringstream is(s);
+        is >> engine_ >> draws_;
+        if (!is) throw std::invalid_argument("malformed Rng state");
+    }
 
 private:
     std::mt19937_64 engine_;
@@ -144,6 +158,7 @@ struct MemoryGauge {     // evolve.hpp:52-71 (live genome accounting)
     void sub(std::int64_t n = 1) { live_ -= n; }
     std::int64_t live() const { return live_; }
     std::int64_t high_water() const { return high_; }
+    void restore(std::int64_t live, std::int64_t high) { live_ = live; high_ = high; }
 private:
     std::int64_t live_ = 0, high_ = 0;
 };

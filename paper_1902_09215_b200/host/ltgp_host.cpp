@@ -376,10 +376,142 @@ void ltgp_host_plan_generation(uint64_t seed, uint32_t M, const ltgp_record* rec
     std::copy(plans.begin(), plans.end(), out);
 }
 
-// run.hpp:33-36 on the engine.
-int64_t ltgp_host_run(ltgp_engine* e, uint32_t M, uint32_t G, uint64_t node_limit, uint32_t k, uint64_t seed,
-                      int grow_mode, uint64_t memory_budget, const char* dump_path, int* reason, uint64_t* nodes,
-                      double* eval_seconds) {
+}  // extern "C"
+
+namespace {
+
+// Checkpoint/resume of a run (a SPEC non-goal kept
+// as an operational feature): the device-resident population, its records,
+// the Rng stream position and the run counters, written after a completed
+// generation. Little-endian binary: Header, the Rng text state, M records
+// {fitness bits, hits, size, depth}, the M genomes back to back (size bytes
+// each, downloaded from the engine), then an FNV-1a 64 of everything before.
+constexpr char kCkptMagic[8] = {'L', 'T', 'G', 'P', 'C', 'K', 'P', '1'};
+
+struct CkptHeader {
+    char magic[8];
+    uint32_t M, k;
+    uint64_t node_limit, seed, memory_budget;
+    int32_t grow_mode;
+    uint32_t rng_len;
+    uint64_t gen, nodes;
+    double secs;
+    int64_t gauge_live, gauge_high;
+};
+
+struct Fnv {
+    uint64_t h = 0xcbf29ce484222325ull;
+    void add(const void* p, size_t n) {
+        const auto* b = static_cast<const uint8_t*>(p);
+        for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 0x100000001b3ull;
+    }
+};
+
+struct CkptWriter {
+    FILE* f;
+    Fnv fnv;
+    void put(const void* p, size_t n) {
+        if (n && std::fwrite(p, 1, n, f) != n) throw std::runtime_error("checkpoint: write failed");
+        fnv.add(p, n);
+    }
+};
+
+struct CkptReader {
+    FILE* f;
+    Fnv fnv;
+    void get(void* p, size_t n) {
+        if (n && std::fread(p, 1, n, f) != n) throw std::invalid_argument("checkpoint: truncated file");
+        fnv.add(p, n);
+    }
+};
+
+void save_checkpoint(const char* path, ltgp_engine* e, const CkptHeader& h0, const Rng& rng,
+                     const std::vector<Individual>& pop) {
+    const std::string tmp = std::string(path) + ".tmp";
+    FILE* f = std::fopen(tmp.c_str(), "wb");
+    if (!f) throw std::runtime_error("checkpoint: cannot open " + tmp);
+    try {
+        CkptWriter w{f, {}};
+        CkptHeader h = h0;
+        const std::string rs = rng.state();
+        h.rng_len = static_cast<uint32_t>(rs.size());
+        w.put(&h, sizeof h);
+        w.put(rs.data(), rs.size());
+        for (const auto& ind : pop) {
+            const ltgp_record r{ind.fitness, ind.hits, ind.size, ind.depth};
+            w.put(&r, sizeof r);
+        }
+        std::vector<uint8_t> buf;
+        for (uint32_t i = 0; i < h.M; ++i) {  // the genomes live on the device
+            buf.resize(pop[i].size);
+            uint64_t n = 0;
+            check(ltgp_download_genome(e, i, buf.data(), buf.size(), &n));
+            if (n != pop[i].size) throw std::runtime_error("checkpoint: genome size mismatch");
+            w.put(buf.data(), buf.size());
+        }
+        const uint64_t sum = w.fnv.h;
+        if (std::fwrite(&sum, 8, 1, f) != 1) throw std::runtime_error("checkpoint: write failed");
+        if (std::fclose(f) != 0) throw std::runtime_error("checkpoint: close failed");
+    } catch (...) {
+        std::fclose(f);
+        std::remove(tmp.c_str());
+        throw;
+    }
+    if (std::rename(tmp.c_str(), path) != 0) throw std::runtime_error("checkpoint: rename failed");
+}
+
+// Loads a checkpoint written by a run with the same parameters (any
+// mismatch is std::invalid_argument, like validate(RunConfig)).
+void load_checkpoint(const char* path, const CkptHeader& want, CkptHeader& h, Rng& rng,
+                     std::vector<Individual>& pop) {
+    FILE* f = std::fopen(path, "rb");
+    if (!f) throw std::invalid_argument(std::string("checkpoint: cannot open ") + path);
+    try {
+        CkptReader r{f, {}};
+        r.get(&h, sizeof h);
+        if (std::memcmp(h.magic, kCkptMagic, 8) != 0) throw std::invalid_argument("checkpoint: bad magic");
+        if (h.M != want.M || h.k != want.k || h.node_limit != want.node_limit || h.seed != want.seed ||
+            h.memory_budget != want.memory_budget || h.grow_mode != want.grow_mode)
+            throw std::invalid_argument("checkpoint: run parameters differ");
+        if (h.rng_len > 1u << 20) throw std::invalid_argument("checkpoint: bad Rng state length");
+        std::string rs(h.rng_len, '\0');
+        r.get(rs.data(), rs.size());
+        rng.set_state(rs);
+        pop.assign(h.M, Individual{});
+        for (auto& ind : pop) {
+            ltgp_record rec;
+            r.get(&rec, sizeof rec);
+            ind.fitness = rec.fitness;
+            ind.hits = rec.hits;
+            ind.size = rec.size;
+            ind.depth = rec.depth;
+        }
+        for (auto& ind : pop) {
+            if (ind.size == 0 || ind.size > h.node_limit) throw std::invalid_argument("checkpoint: bad genome size");
+            std::vector<uint8_t> ops(ind.size);
+            r.get(ops.data(), ops.size());
+            ind.genome = Genome(std::move(ops));
+        }
+        uint64_t sum = 0;
+        if (std::fread(&sum, 8, 1, f) != 1 || sum != r.fnv.h)
+            throw std::invalid_argument("checkpoint: checksum mismatch");
+        std::fclose(f);
+    } catch (...) {
+        std::fclose(f);
+        throw;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+// run.hpp:33-36 on the engine, optionally checkpointed
+// every ckpt_every generations and/or resumed from a checkpoint.
+int64_t ltgp_host_run_checkpointed(ltgp_engine* e, uint32_t M, uint32_t G, uint64_t node_limit, uint32_t k,
+                                   uint64_t seed, int grow_mode, uint64_t memory_budget, const char* dump_path,
+                                   const char* ckpt_path, uint32_t ckpt_every, const char* resume_path,
+                                   int* reason, uint64_t* nodes, double* eval_seconds) {
     try {
         RunConfig cfg;
         cfg.population_size = M;
@@ -389,16 +521,45 @@ int64_t ltgp_host_run(ltgp_engine* e, uint32_t M, uint32_t G, uint64_t node_limi
         cfg.seed = seed;
         cfg.memory_budget_bytes = memory_budget;
         validate(cfg);
+        if (ckpt_every && !ckpt_path) throw std::invalid_argument("ckpt_every without a checkpoint path");
         const TestSuite suite = make_suite(suite_seed(seed));
         Rng rng(seed);
         std::vector<Individual> pop(M), next;
-        auto genomes = ramped_half_and_half(rng, M, node_limit, 2, 6, static_cast<GrowMode>(grow_mode));
-        for (uint32_t i = 0; i < M; ++i) pop[i].genome = std::move(genomes[i]);
         std::vector<WorkerState> pool(1);
         MemoryGauge gauge;
-        gauge.add(M);
         ExecContext ctx{suite, cfg, pool, gauge, e};
-        FILE* dump = dump_path ? std::fopen(dump_path, "w") : nullptr;
+        CkptHeader hdr{};
+        std::memcpy(hdr.magic, kCkptMagic, 8);
+        hdr.M = M;
+        hdr.k = k;
+        hdr.node_limit = node_limit;
+        hdr.seed = seed;
+        hdr.memory_budget = memory_budget;
+        hdr.grow_mode = grow_mode;
+        *reason = 0;
+        *nodes = 0;
+        double secs = 0.0;
+        uint32_t gen0 = 0;
+        if (resume_path) {
+            CkptHeader h;
+            load_checkpoint(resume_path, hdr, h, rng, pop);
+            gauge.restore(h.gauge_live, h.gauge_high);
+            // the parents go back to the device; their records are restored,
+            // not recomputed
+            check(ltgp_set_suite(e, suite.inputs, suite.targets, suite.constants));
+            std::vector<const std::uint8_t*> ptrs(M);
+            std::vector<std::uint64_t> sizes(M);
+            for (uint32_t i = 0; i < M; ++i) {
+                ptrs[i] = pop[i].genome.data();
+                sizes[i] = pop[i].genome.size();
+            }
+            check(ltgp_upload_population(e, M, ptrs.data(), sizes.data()));
+            for (auto& ind : pop) ind.genome.release();
+            gen0 = static_cast<uint32_t>(h.gen);
+            *nodes = h.nodes;
+            secs = h.secs;
+        }
+        FILE* dump = dump_path ? std::fopen(dump_path, resume_path ? "a" : "w") : nullptr;
         auto write_dump = [&](uint32_t gen) {  // stats.hpp:104-107
             if (!dump) return;
             for (uint32_t i = 0; i < M; ++i) {
@@ -408,17 +569,29 @@ int64_t ltgp_host_run(ltgp_engine* e, uint32_t M, uint32_t G, uint64_t node_limi
                 std::fprintf(dump, "%u %u %u %u %d %08x\n", gen, i, pop[i].size, pop[i].depth, pop[i].hits, bits);
             }
         };
-        *reason = 0;
-        *nodes = 0;
-        double secs = 0.0;
+        auto checkpoint = [&](uint32_t gen) {
+            if (!ckpt_path) return;
+            hdr.gen = gen;
+            hdr.nodes = *nodes;
+            hdr.secs = secs;
+            hdr.gauge_live = gauge.live();
+            hdr.gauge_high = gauge.high_water();
+            save_checkpoint(ckpt_path, e, hdr, rng, pop);
+        };
         ltgp_stats st;
-        evaluate_population(pop, ctx);
-        check(ltgp_get_stats(e, &st));
-        secs += st.eval_seconds;
-        for (auto& ind : pop) *nodes += ind.size;
-        write_dump(0);
-        int64_t done = 0;
-        for (uint32_t gen = 1; gen <= G; ++gen) {
+        if (!resume_path) {
+            auto genomes = ramped_half_and_half(rng, M, node_limit, 2, 6, static_cast<GrowMode>(grow_mode));
+            for (uint32_t i = 0; i < M; ++i) pop[i].genome = std::move(genomes[i]);
+            gauge.add(M);
+            evaluate_population(pop, ctx);
+            check(ltgp_get_stats(e, &st));
+            secs += st.eval_seconds;
+            for (auto& ind : pop) *nodes += ind.size;
+            write_dump(0);
+            if (ckpt_every) checkpoint(0);
+        }
+        int64_t done = gen0;
+        for (uint32_t gen = gen0 + 1; gen <= G; ++gen) {
             const auto plans = plan_generation(rng, pop, k);
             const ExecOutcome o = execute_generation(plans, pop, next, ctx);
             if (o.memory_budget_exceeded) { *reason = 2; break; }  // TerminationReason (evolve.hpp:34)
@@ -429,6 +602,7 @@ int64_t ltgp_host_run(ltgp_engine* e, uint32_t M, uint32_t G, uint64_t node_limi
             for (auto& ind : pop) *nodes += ind.size;
             done = gen;
             write_dump(gen);
+            if (ckpt_every && (gen % ckpt_every == 0 || gen == G)) checkpoint(gen);
         }
         if (dump) std::fclose(dump);
         if (eval_seconds) *eval_seconds = secs;
@@ -437,6 +611,13 @@ int64_t ltgp_host_run(ltgp_engine* e, uint32_t M, uint32_t G, uint64_t node_limi
         std::fprintf(stderr, "ltgp_host_run: %s\n", ex.what());
         return -1;
     }
+}
+
+int64_t ltgp_host_run(ltgp_engine* e, uint32_t M, uint32_t G, uint64_t node_limit, uint32_t k, uint64_t seed,
+                      int grow_mode, uint64_t memory_budget, const char* dump_path, int* reason, uint64_t* nodes,
+                      double* eval_seconds) {
+    return ltgp_host_run_checkpointed(e, M, G, node_limit, k, seed, grow_mode, memory_budget, dump_path, nullptr,
+                                      0, nullptr, reason, nodes, eval_seconds);
 }
 
 }  // extern "C"

@@ -263,6 +263,38 @@ def test_run_dump_matches_oracle(oracle, tmp_path, seed, grow):
         assert d.read_bytes() == d_ref.read_bytes()
 
 
+@pytest.mark.parametrize("shards", [1, 2])
+def test_run_checkpoint_resume_matches_oracle(oracle, tmp_path, shards):
+    """Checkpoint/resume: a run checkpointed every 7
+    generations, stopped at generation 20 and resumed in a fresh engine to
+    40, writes the same dump as the oracle's uninterrupted 40 generations;
+    totals (generations, nodes) count the whole run. A checkpoint from a run
+    with other parameters, or a damaged file, is refused."""
+    ref = tmp_path / "ref.txt"
+    r = oracle.run(48, 40, 10**9, 7, 2, 0, str(ref), 1)
+    ck = tmp_path / "run.ckpt"
+    d = tmp_path / "gpu.txt"
+    with ltgp.Engine([0] * shards, node_limit=10**9, chunk_nodes=256) as e:
+        g1 = e.run(48, 20, 10**9, 7, 2, str(d), 1, checkpoint=str(ck), checkpoint_every=7)
+    assert g1["generations"] == 20 and ck.exists()
+    with ltgp.Engine([0] * shards, node_limit=10**9) as e:
+        g2 = e.run(48, 40, 10**9, 7, 2, str(d), 1, resume=str(ck))
+    assert g2["generations"] == r["generations"] == 40
+    assert d.read_bytes() == ref.read_bytes()
+    with ltgp.Engine([0], node_limit=10**9) as e:
+        full = e.run(48, 40, 10**9, 7, 2, None, 1)
+    assert g2["nodes"] == full["nodes"]
+    with ltgp.Engine([0], node_limit=10**9) as e:
+        with pytest.raises(ltgp.EngineError):
+            e.run(48, 40, 10**9, 7, 3, None, 1, resume=str(ck))  # other seed
+        bad = tmp_path / "bad.ckpt"
+        raw = bytearray(ck.read_bytes())
+        raw[len(raw) // 2] ^= 1
+        bad.write_bytes(bytes(raw))
+        with pytest.raises(ltgp.EngineError):
+            e.run(48, 40, 10**9, 7, 2, None, 1, resume=str(bad))
+
+
 def test_run_size_limit_matches_oracle(oracle, tmp_path):
     # SPEC.md:380: node_limit=63 -> SizeLimitHit within a few generations
     r = oracle.run(48, 300, 63, 7, 4, 0, str(tmp_path / "a"))
