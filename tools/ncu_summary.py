@@ -34,6 +34,10 @@ summary = {
     "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
     "dram_bytes_per_node": (rd + wr) / nodes,
     "instructions_per_node": inst / nodes if inst else None,
+    "shared_wavefronts_per_node": get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum") / nodes
+    if "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum" in h else None,
+    "shared_store_bank_conflicts": get("l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum")
+    if "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_st.sum" in h else None,
     "metrics_pct": keep,
 }
 json.dump(summary, open(out, "w"), indent=1)
