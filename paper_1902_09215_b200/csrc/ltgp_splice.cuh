@@ -111,17 +111,35 @@ __global__ void k_child_size(const PlanDev* plans, uint32_t count, const DirEntr
     child_size[c] = mn - (uint64_t)(x.me - x.ms) + (uint64_t)(x.de - x.ds);
 }
 
-__device__ __forceinline__ uint32_t ld_word_unaligned(const uint8_t* p) {
-    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-    const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
-    const uint32_t sh = (uint32_t)(a & 3) * 8;
-    const uint32_t lo = w[0];
-    if (sh == 0) return lo;
-    return __funnelshift_r(lo, w[1], sh);
+// 16 bytes of a parent starting at src (any alignment): the two aligned
+// 16-byte blocks that cover them, read through the non-coherent path (the
+// block shared with the neighbouring thread's chunk hits in L1), then funnel
+// shifts. ws/bs (word and bit offset of src within its block) are the same for
+// every chunk of a segment, so the switch is warp-uniform.
+__device__ __forceinline__ uint4 ld16_unaligned(const uint8_t* src) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+    const uint4* al = reinterpret_cast<const uint4*>(a & ~uintptr_t(15));
+    const uint32_t off = (uint32_t)(a & 15);
+    const uint4 x = __ldg(al);
+    if (off == 0) return x;
+    const uint4 y = __ldg(al + 1);
+    const uint32_t bs = (off & 3) * 8;
+    uint32_t w0, w1, w2, w3, w4;
+    switch (off >> 2) {
+        case 0: w0 = x.x; w1 = x.y; w2 = x.z; w3 = x.w; w4 = y.x; break;
+        case 1: w0 = x.y; w1 = x.z; w2 = x.w; w3 = y.x; w4 = y.y; break;
+        case 2: w0 = x.z; w1 = x.w; w2 = y.x; w3 = y.y; w4 = y.z; break;
+        default: w0 = x.w; w1 = y.x; w2 = y.y; w3 = y.z; w4 = y.w; break;
+    }
+    return make_uint4(__funnelshift_r(w0, w1, bs), __funnelshift_r(w1, w2, bs), __funnelshift_r(w2, w3, bs),
+                      __funnelshift_r(w3, w4, bs));
 }
 
 // One CTA per child; dst offsets are 16-aligned, bytes past the child up to
-// the next 16-byte boundary are set to 0xff (never read as nodes).
+// the next 16-byte boundary are set to 0xff (never read as nodes). Each
+// thread writes 16-byte chunks; a chunk inside one segment is one unaligned
+// 16-byte copy, a chunk that straddles a segment boundary or the child's end
+// (at most three per child) is assembled byte by byte.
 __global__ void __launch_bounds__(256) k_splice(const PlanDev* plans, uint32_t count,
                                                 const DirEntry* dir, const Extent* ext,
                                                 const uint64_t* child_off, const uint64_t* child_size,
@@ -131,31 +149,34 @@ __global__ void __launch_bounds__(256) k_splice(const PlanDev* plans, uint32_t c
         const Extent x = ext[c];
         const uint8_t* mum = dir[p.mum].ptr;
         const uint8_t* dad = dir[p.dad].ptr;
-        const uint64_t mn = dir[p.mum].size;
         const uint64_t b1 = x.ms;                      // end of segment A
         const uint64_t b2 = b1 + (x.de - x.ds);        // end of segment B
         const uint64_t cn = child_size[c];
-        uint32_t* dst = reinterpret_cast<uint32_t*>(arena + child_off[c]);
-        const uint64_t nwords = ((cn + 15) & ~uint64_t(15)) / 4;
-        (void)mn;
-        for (uint64_t w = threadIdx.x; w < nwords; w += blockDim.x) {
-            const uint64_t q = 4 * w;
-            const bool edge = (q < b1 && b1 < q + 4) || (q < b2 && b2 < q + 4) || (q + 4 > cn);
-            uint32_t v;
+        uint4* dst = reinterpret_cast<uint4*>(arena + child_off[c]);
+        const uint64_t nchunks = (cn + 15) / 16;
+        for (uint64_t w = threadIdx.x; w < nchunks; w += blockDim.x) {
+            const uint64_t q = 16 * w;
+            const bool edge = (q < b1 && b1 < q + 16) || (q < b2 && b2 < q + 16) || (q + 16 > cn);
+            uint4 v;
             if (!edge) {
-                const uint8_t* src = q < b1 ? mum + q : q < b2 ? dad + x.ds + (q - b1)
-                                                                : mum + x.me + (q - b2);
-                v = ld_word_unaligned(src);
+                const uint8_t* src = q < b1 ? mum + q : q < b2 ? dad + x.ds + (q - b1) : mum + x.me + (q - b2);
+                v = ld16_unaligned(src);
             } else {
-                v = 0;
+                uint32_t t[4];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const uint64_t pos = q + k;
-                    uint32_t b = 0xffu;
-                    if (pos < cn) b = pos < b1 ? mum[pos] : pos < b2 ? dad[x.ds + (pos - b1)]
-                                                                    : mum[x.me + (pos - b2)];
-                    v |= b << (8 * k);
+                for (int k4 = 0; k4 < 4; ++k4) {
+                    uint32_t word = 0;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint64_t pos = q + 4 * k4 + k;
+                        uint32_t b = 0xffu;
+                        if (pos < cn) b = pos < b1 ? mum[pos] : pos < b2 ? dad[x.ds + (pos - b1)]
+                                                                        : mum[x.me + (pos - b2)];
+                        word |= b << (8 * k);
+                    }
+                    t[k4] = word;
                 }
+                v = make_uint4(t[0], t[1], t[2], t[3]);
             }
             dst[w] = v;
         }
