@@ -255,10 +255,24 @@ def run_ours(args, rank, world, local_rank):
     peak_tops = sms * 128 * pk["sm_max_mhz"] * 1e6 / 1e12  # FP32 lanes/clk x clock, 1 GPop = 1 op
     achieved = nodes_rank * LANES / kern_s / 1e12
     traffic = None
+    binding = None
     prof = os.path.join(ROOT, "profiles", "ncu_k_eval.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            pj = json.load(open(prof))
+            traffic = pj.get("dram_bytes_per_launch")
+            mp = pj.get("metrics_pct", {})
+            # what actually bounds the interpreter: issue
+            # slots and the shared-memory pipe, not the FP32 pipe or HBM
+            binding = {
+                "resource": "instruction issue + shared-memory pipe (per-node dispatch of an interpreter)",
+                "issue_active_pct": float(mp.get("sm__issue_active.avg.pct_of_peak_sustained_elapsed", "nan")),
+                "shared_wavefronts_pct": float(mp.get(
+                    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "nan")),
+                "fma_pipe_pct": float(mp.get("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "nan")),
+                "inst_per_node": pj.get("instructions_per_node"),
+                "shared_wavefronts_per_node": pj.get("shared_wavefronts_per_node"),
+                "source": "profiles/ncu_k_eval.json (ncu --set full of the same k_eval on this workload)"}
         except Exception:
             traffic = None
     line = {
@@ -279,7 +293,7 @@ def run_ours(args, rank, world, local_rank):
                      "note": f"k_eval only: {nodes_rank} nodes x 48 ops / {kern_s * 1e3:.3f} ms avg launch; "
                              f"peak = {sms} SMs x 128 FP32 lanes x {pk['sm_max_mhz']:.0f} MHz ({pk_kind} clock); "
                              f"opcode stream {nodes_rank / kern_s / 1e9:.1f} GB/s of {pk['hbm_gbs']:.0f} GB/s HBM ({pk_kind})",
-                     "combine_ms": float(np.mean(comb)) * 1e3},
+                     "combine_ms": float(np.mean(comb)) * 1e3, "binding": binding},
         "clocks": clk,
     }
     if world == 1 and rank == 0 and not args.no_evolution:

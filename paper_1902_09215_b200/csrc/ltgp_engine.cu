@@ -7,6 +7,8 @@
 // evaluated on the GPU (there is no CPU fallback in this library).
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl is opened at run time (see RecordGather)
 
 #include <algorithm>
 #include <cmath>
@@ -259,6 +261,22 @@ struct ltgp_engine {
     uint64_t memory_budget = 0;  // planned generation bytes allowed (0: no check)
     ltgp_stats stats;
     HostBuf staging;
+    // record all-gather of a multi-shard population: every
+    // shard's records into one n_shards x cmax array on each device
+    struct Gather {
+        bool nccl = false;                       // NCCL across distinct devices
+        void* lib = nullptr;                     // dlopen'ed libnccl.so.2
+        ncclComm_t comms[LTGP_MAX_SHARDS] = {};
+        ncclResult_t (*comm_init_all)(ncclComm_t*, int, const int*) = nullptr;
+        ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+        ncclResult_t (*group_start)() = nullptr;
+        ncclResult_t (*group_end)() = nullptr;
+        ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+        const char* (*error_string)(ncclResult_t) = nullptr;
+        DevBuf send[LTGP_MAX_SHARDS], recv[LTGP_MAX_SHARDS];  // NCCL: per shard; copies: recv[0] only
+        HostBuf h;
+        cudaEvent_t ev[2] = {};
+    } gather;
 };
 
 namespace {
@@ -825,6 +843,116 @@ int upload_tables(Shard& s, TreeSet& ts) {
     return 0;
 }
 
+// Opens NCCL for a population sharded over distinct devices (cfg.use_nccl):
+// one communicator per shard, created in-process by ncclCommInitAll. The
+// library is opened at run time with RTLD_LOCAL (torch may have loaded its
+// own libnccl.so.2 into the process; its soname resolves to that copy).
+int init_gather(ltgp_engine* e) {
+    auto& g = e->gather;
+    const int n = (int)e->shards.size();
+    CK(cudaSetDevice(e->shards[0].dev));
+    CK(cudaEventCreate(&g.ev[0]));
+    CK(cudaEventCreate(&g.ev[1]));
+    bool distinct = n > 1;
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < i; ++j)
+            if (e->shards[i].dev == e->shards[j].dev) distinct = false;
+    if (!e->cfg.use_nccl || !distinct) return 0;
+    g.lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!g.lib) { set_err("use_nccl: cannot open libnccl.so.2: %s", dlerror()); return -1; }
+    g.comm_init_all = reinterpret_cast<decltype(g.comm_init_all)>(dlsym(g.lib, "ncclCommInitAll"));
+    g.all_gather = reinterpret_cast<decltype(g.all_gather)>(dlsym(g.lib, "ncclAllGather"));
+    g.group_start = reinterpret_cast<decltype(g.group_start)>(dlsym(g.lib, "ncclGroupStart"));
+    g.group_end = reinterpret_cast<decltype(g.group_end)>(dlsym(g.lib, "ncclGroupEnd"));
+    g.comm_destroy = reinterpret_cast<decltype(g.comm_destroy)>(dlsym(g.lib, "ncclCommDestroy"));
+    g.error_string = reinterpret_cast<decltype(g.error_string)>(dlsym(g.lib, "ncclGetErrorString"));
+    if (!g.comm_init_all || !g.all_gather || !g.group_start || !g.group_end || !g.comm_destroy || !g.error_string) {
+        set_err("use_nccl: libnccl.so.2 lacks a required symbol");
+        return -1;
+    }
+    int devs[LTGP_MAX_SHARDS];
+    for (int i = 0; i < n; ++i) devs[i] = e->shards[i].dev;
+    const ncclResult_t r = g.comm_init_all(g.comms, n, devs);
+    if (r != ncclSuccess) { set_err("ncclCommInitAll: %s", g.error_string(r)); return -1; }
+    g.nccl = true;
+    return 0;
+}
+
+void release_gather(ltgp_engine* e) {
+    auto& g = e->gather;
+    if (g.nccl)
+        for (size_t i = 0; i < e->shards.size(); ++i) g.comm_destroy(g.comms[i]);
+    for (auto& b : g.send) b.release();
+    for (auto& b : g.recv) b.release();
+    g.h.release();
+    for (auto& ev : g.ev) if (ev) cudaEventDestroy(ev);
+    if (g.lib) dlclose(g.lib);
+    g = ltgp_engine::Gather{};
+}
+
+// All-gather of the shards' 16-byte records after an evaluation (every
+// shard's stream already synchronised): shard s's block lands at
+// [s * cmax, s * cmax + count_s) of an n x cmax array — on every device with
+// NCCL (one grouped ncclAllGather, NVLink), on shard 0's device otherwise
+// (peer copies; shards that repeat a device). Shard 0's array then goes to
+// the host in one copy and is unpacked into slot order.
+int gather_records(ltgp_engine* e, ltgp_record* out) {
+    auto& g = e->gather;
+    const int n = (int)e->shards.size();
+    uint32_t cmax = 1;
+    for (const Shard& s : e->shards) cmax = std::max(cmax, s.count);
+    const size_t blk = sizeof(ltgp_record) * cmax;
+    Shard& s0 = e->shards[0];
+    CK(cudaSetDevice(s0.dev));
+    CK(cudaEventRecord(g.ev[0], s0.st));
+    if (g.nccl) {
+        for (int i = 0; i < n; ++i) {
+            Shard& s = e->shards[i];
+            TRY(g.send[i].ensure(blk, s.dev));
+            TRY(g.recv[i].ensure(blk * n, s.dev));
+            CK(cudaSetDevice(s.dev));
+            if (s.count)
+                CK(cudaMemcpyAsync(g.send[i].p, s.rec.p, sizeof(ltgp_record) * s.count, cudaMemcpyDeviceToDevice,
+                                   s.st));
+        }
+        g.group_start();
+        for (int i = 0; i < n; ++i) {
+            const ncclResult_t r = g.all_gather(g.send[i].p, g.recv[i].p, blk, ncclUint8, g.comms[i], e->shards[i].st);
+            if (r != ncclSuccess) { g.group_end(); set_err("ncclAllGather: %s", g.error_string(r)); return -1; }
+        }
+        const ncclResult_t r = g.group_end();
+        if (r != ncclSuccess) { set_err("ncclGroupEnd: %s", g.error_string(r)); return -1; }
+    } else {
+        TRY(g.recv[0].ensure(blk * n, s0.dev));
+        CK(cudaSetDevice(s0.dev));
+        for (int i = 0; i < n; ++i) {
+            const Shard& s = e->shards[i];
+            if (s.count)
+                CK(cudaMemcpyPeerAsync(g.recv[0].as<uint8_t>() + blk * i, s0.dev, s.rec.p, s.dev,
+                                       sizeof(ltgp_record) * s.count, s0.st));
+        }
+    }
+    CK(cudaSetDevice(s0.dev));
+    CK(cudaEventRecord(g.ev[1], s0.st));
+    TRY(g.h.ensure(blk * n));
+    CK(cudaMemcpyAsync(g.h.p, g.recv[0].p, blk * n, cudaMemcpyDeviceToHost, s0.st));
+    for (int i = 1; i < n && g.nccl; ++i) {  // every device holds the array; wait for all
+        CK(cudaSetDevice(e->shards[i].dev));
+        CK(cudaStreamSynchronize(e->shards[i].st));
+    }
+    CK(cudaSetDevice(s0.dev));
+    CK(cudaStreamSynchronize(s0.st));
+    float ms = 0.0f;
+    CK(cudaEventElapsedTime(&ms, g.ev[0], g.ev[1]));
+    e->stats.gather_seconds = ms * 1e-3;
+    if (out)
+        for (int i = 0; i < n; ++i) {
+            const Shard& s = e->shards[i];
+            std::memcpy(out + s.first, g.h.as<uint8_t>() + blk * i, sizeof(ltgp_record) * s.count);
+        }
+    return 0;
+}
+
 int collect(ltgp_engine* e, ltgp_record* out, float* outs48) {
     double secs = 0.0, ksecs = 0.0, csecs = 0.0;
     uint64_t nodes = 0, chunks = 0, reruns = 0, exits = 0, adjusts = 0, steps = 0;
@@ -833,8 +961,9 @@ int collect(ltgp_engine* e, ltgp_record* out, float* outs48) {
         CK(cudaSetDevice(s.dev));
         CK(cudaStreamSynchronize(s.st));
         TRY(finish_eval(e, s));
-        if (out) CK(cudaMemcpyAsync(out + s.first, s.rec.p, sizeof(ltgp_record) * s.count,
-                                    cudaMemcpyDeviceToHost, s.st));
+        if (out && e->shards.size() == 1)
+            CK(cudaMemcpyAsync(out + s.first, s.rec.p, sizeof(ltgp_record) * s.count,
+                               cudaMemcpyDeviceToHost, s.st));
         if (outs48) CK(cudaMemcpyAsync(outs48 + (size_t)s.first * kLanes, s.outs.p,
                                        sizeof(float) * kLanes * s.count, cudaMemcpyDeviceToHost, s.st));
         CK(cudaStreamSynchronize(s.st));
@@ -856,6 +985,7 @@ int collect(ltgp_engine* e, ltgp_record* out, float* outs48) {
         adjusts += s.h_counters.as<uint32_t>()[5];
         steps += s.last_steps;
     }
+    if (e->shards.size() > 1) TRY(gather_records(e, out));
     e->stats.last_spine_steps = steps;
     e->stats.last_exits = exits;
     e->stats.last_window_adjusts = adjusts;
@@ -917,6 +1047,11 @@ int ltgp_engine_create(const ltgp_config* cfg, ltgp_engine** out) {
             }
             cudaGetLastError();
         }
+    if (init_gather(e.get()) != 0) {
+        release_gather(e.get());
+        for (auto& s : e->shards) s.release();
+        return -1;
+    }
     *out = e.release();
     return 0;
 }
@@ -928,6 +1063,7 @@ int ltgp_engine_destroy(ltgp_engine* e) {
         if (s.st) cudaStreamSynchronize(s.st);
         s.release();
     }
+    release_gather(e);
     e->staging.release();
     delete e;
     return 0;

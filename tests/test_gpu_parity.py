@@ -402,6 +402,12 @@ def test_streamed_evaluate_packed_matches_resident(oracle, suite):
         assert e.evaluate_population().tobytes() == exp.tobytes()  # population = the streamed one
     with engine(suite, devices=(0, 0)) as e:
         assert e.evaluate_packed(buf, offs, sizes).tobytes() == exp.tobytes()
+    # three shards: the records come back through the engine's all-gather
+    # (peer copies into shard 0's n x cmax array; NCCL on distinct devices)
+    with engine(suite, devices=(0, 0, 0)) as e:
+        e.upload_packed(buf, offs, sizes)
+        assert e.evaluate_population().tobytes() == exp.tobytes()
+        assert e.stats()["gather_seconds"] > 0
     # and against the oracle on a sample of slots
     idx = np.arange(0, 4000, 97)
     sub = [buf[int(offs[k]):int(offs[k]) + int(sizes[k])].copy() for k in idx]

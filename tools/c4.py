@@ -11,6 +11,9 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1902_09215_b200 as ltgp  # noqa: E402
 
+if os.environ.get("LTGP_CUDA_LIB"):  # a variant from tools/build_variant.py
+    ltgp.CUDA_LIB_PATH = os.environ["LTGP_CUDA_LIB"]
+
 
 def main():
     ap = argparse.ArgumentParser()
