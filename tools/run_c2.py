@@ -21,12 +21,16 @@ def main():
     ap.add_argument("--oracle", action="store_true")
     ap.add_argument("--grow", type=int, default=1, help="0: SPEC grow (runs collapse), 1: 50/50 grow (runs bloat)")
     ap.add_argument("--dump", default="/tmp/c2_gpu.txt", help="generation dump path ('' for none)")
+    ap.add_argument("--checkpoint", default="", help="checkpoint file (written every --every generations)")
+    ap.add_argument("--every", type=int, default=0)
+    ap.add_argument("--resume", default="", help="continue the run from this checkpoint")
     a = ap.parse_args()
     if a.oracle and not a.dump:
         ap.error("--oracle compares generation dumps: give --dump a path")
     with ltgp.Engine([0] * a.shards, node_limit=a.limit) as e:
         t = time.perf_counter()
-        r = e.run(a.pop, a.gens, a.limit, 7, a.seed, a.dump or None, a.grow)
+        r = e.run(a.pop, a.gens, a.limit, 7, a.seed, a.dump or None, a.grow,
+                  checkpoint=a.checkpoint or None, checkpoint_every=a.every, resume=a.resume or None)
         wall = time.perf_counter() - t
     print(f"engine: {r['generations']} gens, reason {r['reason']}, {r['nodes']} nodes, eval {r['eval_seconds']:.3f} s "
           f"({r['nodes'] * 48 / max(r['eval_seconds'], 1e-9) / 1e12:.3f} T GPops/s eval), wall {wall:.2f} s "
