@@ -76,6 +76,27 @@ int64_t ltgp_host_run_checkpointed(ltgp_engine* e, uint32_t M, uint32_t max_gene
                                    const char* resume_path, int* reason, uint64_t* nodes_evaluated,
                                    double* eval_seconds);
 
+/* BenchCell (bench.hpp:17-27) of run_bench on the engine: workers = GPUs
+   (devices 0..workers-1); batch_gpops = one GPU, parallel_gpops = `workers`
+   GPUs, device-timed, best of `repeats`. The engine has no CPU interpreter:
+   scalar_gpops and vector_speedup are 0. */
+typedef struct {
+    uint64_t tree_size;
+    uint32_t workers;
+    uint64_t nodes;
+    double scalar_gpops, batch_gpops, parallel_gpops, vector_speedup, parallel_speedup;
+    int counters_consistent;
+} ltgp_bench_cell;
+
+/* run_bench (bench.hpp:33-35): for each tree size (made odd) a corpus of
+   ceil(min_corpus_nodes / size) random_tree_of_size trees (tree i from
+   Rng(tree_seed(seed, i))), the Sextic suite of suite_seed(seed), one cell
+   per (size, worker count) in that order into out[n_sizes * n_workers].
+   0 ok, -1 on invalid arguments or an engine error. */
+int ltgp_host_run_bench(const uint64_t* tree_sizes, uint32_t n_sizes, const uint32_t* worker_counts,
+                        uint32_t n_workers, uint64_t seed, uint64_t min_corpus_nodes, int repeats,
+                        ltgp_bench_cell* out);
+
 #ifdef __cplusplus
 }
 #endif

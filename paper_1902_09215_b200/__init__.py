@@ -35,6 +35,9 @@ GEN_STATS_DTYPE = np.dtype([("best_index", "<u4"), ("best_fitness", "<f4"), ("be
                             ("max_size", "<u4"), ("pad", "<u4"), ("sum_size", "<u8"), ("sum_depth", "<u8"),
                             ("sum_fitness", "<f8")])
 PLAN_DTYPE = np.dtype([("mum_index", "<u4"), ("dad_index", "<u4"), ("mum_pt", "<u4"), ("dad_pt", "<u4")])
+BENCH_CELL_DTYPE = np.dtype([("tree_size", "<u8"), ("workers", "<u4"), ("nodes", "<u8"), ("scalar_gpops", "<f8"),
+                             ("batch_gpops", "<f8"), ("parallel_gpops", "<f8"), ("vector_speedup", "<f8"),
+                             ("parallel_speedup", "<f8"), ("counters_consistent", "<i4")], align=True)
 
 
 class EngineError(RuntimeError):
@@ -100,6 +103,7 @@ _HOST_SIGS = {
     "ltgp_host_run": (C.c_int64, [_P, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint64, C.c_int, C.c_uint64,
                                   C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_uint64),
                                   C.POINTER(C.c_double)]),
+    "ltgp_host_run_bench": (C.c_int, [_P, C.c_uint32, _P, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int, _P]),
     "ltgp_host_run_checkpointed": (C.c_int64, [_P, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint64,
                                                C.c_int, C.c_uint64, C.c_char_p, C.c_char_p, C.c_uint32,
                                                C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_uint64),
@@ -231,6 +235,20 @@ def plan_generation(seed: int, records: np.ndarray, k: int = 7) -> np.ndarray:
     records = np.ascontiguousarray(records, RECORD_DTYPE)
     out = np.zeros(len(records), PLAN_DTYPE)
     host_lib().ltgp_host_plan_generation(seed, len(records), _ptr(records), k, _ptr(out))
+    return out
+
+
+def run_bench(tree_sizes, worker_counts=(1,), seed: int = 1, min_corpus_nodes: int = 4_000_000,
+              repeats: int = 3) -> np.ndarray:
+    """run_bench (bench.hpp:33-35) on the engine: one BenchCell per (tree
+    size, GPU count); see include/ltgp_host.h."""
+    ts = np.ascontiguousarray(tree_sizes, np.uint64)
+    wc = np.ascontiguousarray(worker_counts, np.uint32)
+    out = np.zeros(ts.size * wc.size, BENCH_CELL_DTYPE)
+    st = host_lib().ltgp_host_run_bench(_ptr(ts), ts.size, _ptr(wc), wc.size, seed, min_corpus_nodes, repeats,
+                                        _ptr(out))
+    if st != 0:
+        raise EngineError(_err() or "ltgp_host_run_bench failed")
     return out
 
 

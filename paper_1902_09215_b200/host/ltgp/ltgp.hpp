@@ -192,6 +192,30 @@ void evaluate_population(std::vector<Individual>& population, ExecContext ctx);
 ExecOutcome execute_generation(std::span<const CrossoverPlan> plans, std::vector<Individual>& parents,
                                std::vector<Individual>& children, ExecContext ctx);
 
+// bench.hpp:17-35 on the engine. A cell's `workers` is a GPU count (devices
+// 0..workers-1, the population sharded over them); batch_gpops is one GPU
+// and parallel_gpops `workers` GPUs, both device-timed evaluations of the
+// whole corpus (best of `repeats`). The engine has no CPU interpreter, so
+// scalar_gpops and vector_speedup stay 0 (the reference's CPU columns are the
+// oracle's, timed by bench.py's cpu_baseline). counters_consistent: the
+// engine's node counter advanced by exactly the corpus size per evaluation.
+struct BenchCell {
+    std::size_t tree_size = 0;
+    std::uint32_t workers = 0;
+    std::uint64_t nodes = 0;
+    double scalar_gpops = 0.0;
+    double batch_gpops = 0.0;
+    double parallel_gpops = 0.0;
+    double vector_speedup = 0.0;
+    double parallel_speedup = 0.0;
+    bool counters_consistent = false;
+};
+struct BenchReport {
+    std::vector<BenchCell> cells;
+};
+BenchReport run_bench(const std::vector<std::size_t>& tree_sizes, const std::vector<std::uint32_t>& worker_counts,
+                      std::uint64_t seed, std::size_t min_corpus_nodes, int repeats);
+
 // Throws std::runtime_error with ltgp_last_error() on an engine failure.
 void check(int status);
 

@@ -245,6 +245,86 @@ ExecOutcome execute_generation(std::span<const CrossoverPlan> plans, std::vector
     return ExecOutcome{false, false};
 }
 
+namespace {
+struct EngineHandle {  // RAII over ltgp_engine_create / destroy
+    ltgp_engine* e = nullptr;
+    explicit EngineHandle(std::uint32_t gpus) {
+        ltgp_config cfg{};
+        cfg.n_shards = static_cast<int>(gpus);
+        for (std::uint32_t i = 0; i < gpus; ++i) cfg.devices[i] = static_cast<int>(i);
+        cfg.node_limit = std::numeric_limits<std::uint64_t>::max();
+        cfg.use_nccl = 1;
+        check(ltgp_engine_create(&cfg, &e));
+    }
+    ~EngineHandle() { ltgp_engine_destroy(e); }
+    EngineHandle(const EngineHandle&) = delete;
+    EngineHandle& operator=(const EngineHandle&) = delete;
+};
+
+// Best-of-`repeats` device throughput of one corpus on `gpus` GPUs; sets
+// `consistent` if the engine's node counter moved by the corpus size each time.
+double corpus_gpops(std::uint32_t gpus, const TestSuite& suite, const std::vector<std::uint8_t>& buf,
+                    const std::vector<std::uint64_t>& offs, const std::vector<std::uint64_t>& sizes,
+                    std::uint64_t nodes, int repeats, bool& consistent) {
+    EngineHandle h(gpus);
+    check(ltgp_set_suite(h.e, suite.inputs, suite.targets, suite.constants));
+    const auto M = static_cast<std::uint32_t>(sizes.size());
+    check(ltgp_upload_packed(h.e, M, buf.data(), buf.size(), offs.data(), sizes.data()));
+    std::vector<ltgp_record> rec(M);
+    check(ltgp_evaluate_population(h.e, rec.data(), nullptr));  // warm-up
+    double best = 0.0;
+    for (int r = 0; r < std::max(1, repeats); ++r) {
+        ltgp_stats a, b;
+        check(ltgp_get_stats(h.e, &a));
+        std::uint64_t n = 0;
+        check(ltgp_evaluate_population(h.e, rec.data(), &n));
+        check(ltgp_get_stats(h.e, &b));
+        consistent = consistent && n == nodes && b.nodes_evaluated - a.nodes_evaluated == nodes;
+        for (const auto& x : rec) consistent = consistent && x.size > 0;
+        if (b.eval_seconds > 0.0) best = std::max(best, static_cast<double>(nodes) * kLaneWidth / b.eval_seconds);
+    }
+    return best;
+}
+}  // namespace
+
+BenchReport run_bench(const std::vector<std::size_t>& tree_sizes, const std::vector<std::uint32_t>& worker_counts,
+                      std::uint64_t seed, std::size_t min_corpus_nodes, int repeats) {
+    if (tree_sizes.empty() || worker_counts.empty()) throw std::invalid_argument("run_bench: empty grid");
+    for (const std::uint32_t w : worker_counts)  // more GPUs than present: ltgp_engine_create reports it
+        if (w == 0 || w > LTGP_MAX_SHARDS) throw std::invalid_argument("run_bench: worker count (GPUs) out of range");
+    BenchReport report;
+    const TestSuite suite = make_suite(suite_seed(seed));
+    for (const std::size_t size0 : tree_sizes) {
+        if (size0 == 0) throw std::invalid_argument("run_bench: tree size 0");
+        const std::uint64_t n = size0 | 1u;  // random_tree_of_size needs an odd count
+        const std::uint64_t count = std::max<std::uint64_t>(1, (min_corpus_nodes + n - 1) / n);
+        std::vector<std::uint64_t> sizes(count, n), offs(count);
+        const std::uint64_t stride = (n + 15) & ~std::uint64_t(15);
+        std::vector<std::uint8_t> buf(stride * count, 0xff);
+        for (std::uint64_t i = 0; i < count; ++i) {
+            offs[i] = stride * i;
+            Rng r(ltgp_host_tree_seed(seed, static_cast<std::uint32_t>(i)));
+            random_tree_of_size(r, n, buf.data() + offs[i]);
+        }
+        const std::uint64_t nodes = n * count;
+        bool c1 = true;
+        const double batch = corpus_gpops(1, suite, buf, offs, sizes, nodes, repeats, c1);
+        for (const std::uint32_t w : worker_counts) {
+            BenchCell cell;
+            cell.tree_size = n;
+            cell.workers = w;
+            cell.nodes = nodes;
+            cell.batch_gpops = batch;
+            bool cw = c1;
+            cell.parallel_gpops = w == 1 ? batch : corpus_gpops(w, suite, buf, offs, sizes, nodes, repeats, cw);
+            cell.parallel_speedup = batch > 0.0 ? cell.parallel_gpops / batch : 0.0;
+            cell.counters_consistent = cw;
+            report.cells.push_back(cell);
+        }
+    }
+    return report;
+}
+
 }  // namespace ltgp
 
 using namespace ltgp;
@@ -609,6 +689,27 @@ int64_t ltgp_host_run_checkpointed(ltgp_engine* e, uint32_t M, uint32_t G, uint6
         return done;
     } catch (const std::exception& ex) {
         std::fprintf(stderr, "ltgp_host_run: %s\n", ex.what());
+        return -1;
+    }
+}
+
+int ltgp_host_run_bench(const uint64_t* tree_sizes, uint32_t n_sizes, const uint32_t* worker_counts,
+                        uint32_t n_workers, uint64_t seed, uint64_t min_corpus_nodes, int repeats,
+                        ltgp_bench_cell* out) {
+    try {
+        if (!tree_sizes || !worker_counts || !out) throw std::invalid_argument("null argument");
+        const std::vector<std::size_t> ts(tree_sizes, tree_sizes + n_sizes);
+        const std::vector<std::uint32_t> wc(worker_counts, worker_counts + n_workers);
+        const BenchReport r = run_bench(ts, wc, seed, min_corpus_nodes, repeats);
+        for (std::size_t i = 0; i < r.cells.size(); ++i) {
+            const BenchCell& c = r.cells[i];
+            out[i] = ltgp_bench_cell{c.tree_size, c.workers, c.nodes, c.scalar_gpops, c.batch_gpops,
+                                     c.parallel_gpops, c.vector_speedup, c.parallel_speedup,
+                                     c.counters_consistent ? 1 : 0};
+        }
+        return 0;
+    } catch (const std::exception& ex) {
+        std::fprintf(stderr, "ltgp_host_run_bench: %s\n", ex.what());
         return -1;
     }
 }

@@ -55,6 +55,25 @@ def test_no_gpu_fails_loudly():
         ltgp.Engine([0])
 
 
+def test_bench_cell_layout_matches_header(tmp_path):
+    """BENCH_CELL_DTYPE has ltgp_bench_cell's C layout (include/ltgp_host.h)."""
+    import subprocess
+    import paper_1902_09215_b200 as ltgp
+    src = tmp_path / "cell.c"
+    src.write_text(
+        '#include <stddef.h>\n#include <stdio.h>\n#include "ltgp_host.h"\n'
+        'int main(void){printf("%zu %zu %zu %zu\\n", sizeof(ltgp_bench_cell), offsetof(ltgp_bench_cell, nodes),'
+        ' offsetof(ltgp_bench_cell, parallel_speedup), offsetof(ltgp_bench_cell, counters_consistent));'
+        ' return 0;}\n')
+    exe = tmp_path / "cell"
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    subprocess.run(["gcc", "-I", inc, str(src), "-o", str(exe)], check=True)
+    got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    d = ltgp.BENCH_CELL_DTYPE
+    assert got == [d.itemsize, d.fields["nodes"][1], d.fields["parallel_speedup"][1],
+                   d.fields["counters_consistent"][1]]
+
+
 def test_struct_layouts_match_header(tmp_path):
     """The ctypes/numpy views of ltgp_record and ltgp_gen_stats have the C
     layout (offsets compiled from include/ltgp_cuda.h)."""

@@ -548,3 +548,17 @@ def test_error_behaviour_and_edge_cases(oracle, suite):
         e.upload_population([np.array([X], np.uint8)])
         with pytest.raises(ltgp.EngineError, match="set_suite"):
             e.evaluate_population()
+
+
+def test_run_bench_cells():
+    """run_bench (bench.hpp:33-35) on the engine: one cell per (size, GPU
+    count) with consistent node counters and a positive device throughput."""
+    cells = ltgp.run_bench([1001, 20000], [1], seed=1, min_corpus_nodes=200_000, repeats=2)
+    assert cells["tree_size"].tolist() == [1001, 20001]
+    assert cells["nodes"].tolist() == [1001 * 200, 20001 * 10]
+    assert (cells["counters_consistent"] == 1).all()
+    assert (cells["batch_gpops"] > 0).all() and (cells["parallel_gpops"] == cells["batch_gpops"]).all()
+    assert (cells["scalar_gpops"] == 0).all()
+    with pytest.raises(ltgp.EngineError):
+        ltgp.run_bench([1001], [0])
+
