@@ -265,7 +265,9 @@ def run_ours(args, rank, world, local_rank):
             # what actually bounds the interpreter: issue
             # slots and the shared-memory pipe, not the FP32 pipe or HBM
             binding = {
-                "resource": "instruction issue + shared-memory pipe (per-node dispatch of an interpreter)",
+                "resource": "latency of the interpreter's per-pair dispatch chain (LDS record -> jump-table LDC -> "
+                            "BRX): 41% of k_eval's stall samples (profiles/r01_keval_stalls.txt); throughput follows "
+                            "resident warps; issue and shared-memory pipe shown below are not saturated",
                 "issue_active_pct": float(mp.get("sm__issue_active.avg.pct_of_peak_sustained_elapsed", "nan")),
                 "shared_wavefronts_pct": float(mp.get(
                     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "nan")),
