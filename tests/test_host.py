@@ -63,3 +63,25 @@ def test_plan_generation_matches_oracle(oracle):
         b = oracle.plan_generation(seed, rec, 7)
         assert a.tobytes() == b.tobytes()
         assert np.all(a["mum_pt"] < rec["size"][a["mum_index"]])
+
+
+def test_checkpoint_file_validation_without_gpu(tmp_path):
+    """A resume file is validated before the engine is touched: missing,
+    truncated or foreign files are refused (the run returns an error), so a
+    damaged checkpoint can never half-restore a run."""
+    import ctypes as C
+    lib = ltgp.host_lib()
+    reason, nodes, secs = C.c_int(), C.c_uint64(), C.c_double()
+
+    def resume(path):
+        return lib.ltgp_host_run_checkpointed(None, 48, 10, 10**9, 7, 1, 1, 0, None, None, 0, str(path).encode(),
+                                              C.byref(reason), C.byref(nodes), C.byref(secs))
+
+    assert resume(tmp_path / "missing.ckpt") == -1
+    (tmp_path / "short.ckpt").write_bytes(b"LTGPCKP1")
+    assert resume(tmp_path / "short.ckpt") == -1
+    (tmp_path / "foreign.ckpt").write_bytes(b"NOTACKPT" + bytes(200))
+    assert resume(tmp_path / "foreign.ckpt") == -1
+    # ckpt_every without a path is a configuration error
+    assert lib.ltgp_host_run_checkpointed(None, 48, 10, 10**9, 7, 1, 1, 0, None, None, 5, None,
+                                          C.byref(reason), C.byref(nodes), C.byref(secs)) == -1
