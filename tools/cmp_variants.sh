@@ -7,5 +7,6 @@ for v in "$@"; do
   echo "== $v"
   LTGP_CUDA_LIB=$L python tools/prof_c3.py 3 | tail -1
   [ -n "$CMP_EVOLVED" ] && LTGP_CUDA_LIB=$L python tools/evolved_pop.py 3000 | tail -1
+  [ -n "$CMP_EVO200" ] && LTGP_CUDA_LIB=$L python tools/evolved_pop.py 200 | tail -1
   [ -n "$CMP_C4" ] && LTGP_CUDA_LIB=$L python tools/c4.py --reps 2 --check 1 2>&1 | tail -2
 done
