@@ -58,9 +58,9 @@ typedef struct {
 typedef struct {
     uint64_t nodes_evaluated;   /* sum of sizes over all evaluations */
     double eval_seconds;        /* device time of the last evaluation (CUDA events) */
-    double eval_kernel_seconds; /* of which the chunk/tree scan kernel (k_eval) */
+    double eval_kernel_seconds; /* of which the scan pass: k_decode + k_plan + k_eval (+ overflow re-runs) */
     double combine_seconds;     /* of which the spine combine kernel (k_combine) */
-    double splice_seconds;      /* device time of the last extent+splice */
+    double splice_seconds;      /* device time of the last splice (k_splice) */
     double gather_seconds;      /* device time of the last record all-gather */
     uint64_t arena_high_water;  /* bytes, max over shards */
     uint64_t last_chunks;       /* chunk work items of the last evaluation */
@@ -69,6 +69,8 @@ typedef struct {
     uint64_t last_window_adjusts; /* of which needed a stack window spill or refill */
     uint64_t last_spine_steps;  /* spine steps the chunk summaries of the last evaluation hold */
     uint32_t kernel_launches;   /* engine kernels launched by the last call */
+    uint32_t pad0;
+    double keval_seconds;       /* k_eval alone, max over shards (resident evaluations; 0 when streamed) */
 } ltgp_stats;
 
 /* Generation statistics of the current population (GenerationStats,

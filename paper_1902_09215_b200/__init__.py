@@ -56,7 +56,7 @@ class _Stats(C.Structure):
                 ("arena_high_water", C.c_uint64), ("last_chunks", C.c_uint64),
                 ("last_fallback_items", C.c_uint64), ("last_exits", C.c_uint64),
                 ("last_window_adjusts", C.c_uint64), ("last_spine_steps", C.c_uint64),
-                ("kernel_launches", C.c_uint32)]
+                ("kernel_launches", C.c_uint32), ("pad0", C.c_uint32), ("keval_seconds", C.c_double)]
 
 
 _cuda = None

@@ -202,9 +202,11 @@ struct Shard {
     std::vector<uint32_t> items_slices;         // work-list cache key (slice tree boundaries)
     DevBuf xspill[kComputeStreams];             // spill areas of xs[1..] (xs[0] uses spill)
     cudaEvent_t ev[8] = {};
+    cudaEvent_t kev[2] = {};                    // around k_eval of a resident evaluation
     int sms = 0;
     int eval_grid = 0;
     uint32_t first = 0, count = 0;  // global slot range
+    bool kev_valid = false;         // kev bracket the last evaluation's k_eval
     TreeSet set[2];
     int cur = 0;
     TreeSet scratch;                // ltgp_eval_one
@@ -244,6 +246,7 @@ struct Shard {
         for (int k = 1; k < kComputeStreams; ++k) if (xs[k]) cudaStreamDestroy(xs[k]);
         if (cst) cudaStreamDestroy(cst);
         for (auto& e : ev) if (e) cudaEventDestroy(e);
+        for (auto& e : kev) if (e) cudaEventDestroy(e);
         for (auto& e : sev) if (e) cudaEventDestroy(e);
     }
 };
@@ -306,6 +309,7 @@ int init_shard(ltgp_engine* e, Shard& s) {
     for (int k = 1; k < kComputeStreams; ++k) CK(cudaStreamCreateWithFlags(&s.xs[k], cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&s.cst, cudaStreamNonBlocking));
     for (auto& ev : s.ev) CK(cudaEventCreate(&ev));
+    for (auto& ev : s.kev) CK(cudaEventCreate(&ev));
     s.sev.resize(3 * kMaxSlices);
     for (auto& ev : s.sev) CK(cudaEventCreateWithFlags(&ev, trace_slices() ? cudaEventDefault : cudaEventDisableTiming));
     cudaDeviceProp prop;
@@ -555,6 +559,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     if (streamed)
         for (int k = 1; k < kComputeStreams && k < (int)G; ++k) TRY(s.xspill[k].ensure(s.spill.bytes, s.dev));
     CK(cudaEventRecord(s.ev[0], s.st));
+    s.kev_valid = false;
     uint32_t launches = 0;
     for (uint32_t g = 0; g < G; ++g) {
         const uint32_t xk = g % kComputeStreams;
@@ -612,8 +617,11 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             ag.queue = s.counters.as<uint32_t>() + kQueueBase + g;
             if (xk) ag.spill = s.xspill[xk].as<float2>();
             const int grid = std::min<int>(s.eval_grid, (int)ni);
+            if (!streamed) CK(cudaEventRecord(s.kev[0], X));
             K_EVAL<<<std::max(grid, 1), kWarps * 32, eval_smem_bytes(), X>>>(ag, e->suite);
             CK(cudaGetLastError());
+            if (!streamed) CK(cudaEventRecord(s.kev[1], X));
+            s.kev_valid = !streamed;
             DEBUG_SYNC(X, "k_eval");
             ++launches;
         }
@@ -954,7 +962,7 @@ int gather_records(ltgp_engine* e, ltgp_record* out) {
 }
 
 int collect(ltgp_engine* e, ltgp_record* out, float* outs48) {
-    double secs = 0.0, ksecs = 0.0, csecs = 0.0;
+    double secs = 0.0, ksecs = 0.0, csecs = 0.0, kev = 0.0;
     uint64_t nodes = 0, chunks = 0, reruns = 0, exits = 0, adjusts = 0, steps = 0;
     for (Shard& s : e->shards) {
         if (!s.count) continue;
@@ -974,6 +982,10 @@ int collect(ltgp_engine* e, ltgp_record* out, float* outs48) {
         const double k = ms * 1e-3 + s.rerun_ksecs;
         CK(cudaEventElapsedTime(&ms, s.ev[4], s.ev[1]));
         const double cmb = ms * 1e-3 + s.rerun_csecs;
+        if (s.kev_valid) {
+            CK(cudaEventElapsedTime(&ms, s.kev[0], s.kev[1]));
+            kev = std::max(kev, (double)ms * 1e-3);
+        }
         secs = std::max(secs, k + cmb);
         ksecs = std::max(ksecs, k);
         csecs = std::max(csecs, cmb);
@@ -993,6 +1005,7 @@ int collect(ltgp_engine* e, ltgp_record* out, float* outs48) {
     e->stats.eval_seconds = secs;
     e->stats.eval_kernel_seconds = ksecs;
     e->stats.combine_seconds = csecs;
+    e->stats.keval_seconds = kev;
     e->stats.nodes_evaluated += nodes;
     e->stats.last_chunks = chunks;
     return 0;

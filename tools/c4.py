@@ -44,7 +44,8 @@ def main():
             rec, outs = e.evaluate_outputs()
             st = e.stats()
             tot = a.trees * n
-            print(f"eval {st['eval_seconds']*1e3:.1f} ms (k_eval {st['eval_kernel_seconds']*1e3:.1f}, combine "
+            print(f"eval {st['eval_seconds']*1e3:.1f} ms (decode+plan+k_eval {st['eval_kernel_seconds']*1e3:.1f}, k_eval alone "
+                  f"{st['keval_seconds']*1e3:.1f}, combine "
                   f"{st['combine_seconds']*1e3:.1f}) {tot*48/st['eval_seconds']/1e12:.3f} T GPops/s, chunks "
                   f"{st['last_chunks']}, reruns {st['last_fallback_items']}, exits {st['last_exits']}, "
                   f"adjusts {st['last_window_adjusts']}, spine steps {st['last_spine_steps']}", flush=True)

@@ -16,6 +16,6 @@ with ltgp.Engine([0], node_limit=2**62) as e:
         st = e.stats()
         n = int(rec["size"].sum())
         print(f"gen {G}: {n} nodes (mean {n/4000:.0f}, max depth {rec['depth'].max()}), eval {st['eval_seconds']*1e3:.3f} ms "
-              f"(k_eval {st['eval_kernel_seconds']*1e3:.3f}), {n*48/st['eval_seconds']/1e12:.3f} T GPops/s, "
+              f"(decode+plan+k_eval {st['eval_kernel_seconds']*1e3:.3f}, k_eval alone {st['keval_seconds']*1e3:.3f}), {n*48/st['eval_seconds']/1e12:.3f} T GPops/s, "
               f"combine {st['combine_seconds']*1e3:.3f} ms, chunks {st['last_chunks']}, spine steps {st['last_spine_steps']}, "
               f"exits {st['last_exits']}, adjusts {st['last_window_adjusts']}", flush=True)

@@ -23,7 +23,7 @@ def main():
             rec = e.evaluate_population()
             st = e.stats()
             print(f"{sizes.sum()} nodes: {st['eval_seconds']*1e3:.3f} ms device "
-                  f"(k_eval {st['eval_kernel_seconds']*1e3:.3f} ms, combine {st['combine_seconds']*1e3:.3f} ms), "
+                  f"(decode+plan+k_eval {st['eval_kernel_seconds']*1e3:.3f} ms, k_eval alone {st['keval_seconds']*1e3:.3f} ms, combine {st['combine_seconds']*1e3:.3f} ms), "
                   f"{sizes.sum()*48/st['eval_seconds']/1e12:.3f} TGPops/s, wall {1e3*(time.perf_counter()-t):.1f} ms, "
                   f"chunks {st['last_chunks']}, exits {st['last_exits']}, window adjusts {st['last_window_adjusts']}", flush=True)
         assert rec["hits"].min() >= 0
