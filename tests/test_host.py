@@ -85,3 +85,12 @@ def test_checkpoint_file_validation_without_gpu(tmp_path):
     # ckpt_every without a path is a configuration error
     assert lib.ltgp_host_run_checkpointed(None, 48, 10, 10**9, 7, 1, 1, 0, None, None, 5, None,
                                           C.byref(reason), C.byref(nodes), C.byref(secs)) == -1
+
+
+def test_run_bench_argument_validation_without_gpu():
+    """run_bench (bench.hpp:33-35) rejects an empty grid and GPU counts of 0
+    or above LTGP_MAX_SHARDS before creating any engine."""
+    import pytest
+    for sizes, workers in (([], [1]), ([1001], []), ([1001], [0]), ([1001], [17])):
+        with pytest.raises(ltgp.EngineError):
+            ltgp.run_bench(sizes, workers, min_corpus_nodes=1000, repeats=1)
