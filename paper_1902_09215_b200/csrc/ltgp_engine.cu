@@ -579,7 +579,14 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             p_hi = (sl.dst + sl.len + 15) / 16;
         }
         const uint32_t i0 = s.slice_items[g], ni = s.slice_items[g + 1] - i0;
-        if (p_hi > p_lo) {
+        // k_plan_warp (a warp per item, lane-parallel replay between window
+        // adjustments) beats k_plan (a thread per item) on every measured
+        // population (config 3: 14.13 vs 14.20 ms per evaluation; an evolved
+        // 15.6M-node population: 0.66 vs 0.72 ms); LTGP_PLAN=0 selects k_plan.
+        // k_plan_warp also decodes the packets it plans (no k_decode pass).
+        static const int plan_mode = std::getenv("LTGP_PLAN") ? std::atoi(std::getenv("LTGP_PLAN")) : 1;
+        const bool plan_warp = plan_mode != 0;
+        if (p_hi > p_lo && !plan_warp) {
             const uint64_t blocks = std::min<uint64_t>((p_hi - p_lo + 255) / 256, (uint64_t)s.sms * 16);
             k_decode<<<(unsigned)blocks, 256, 0, X>>>(ts.arena.as<uint4>(), dec, ts.meta.as<uint32_t>(), packets,
                                                      p_lo, p_hi);
@@ -587,16 +594,10 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             DEBUG_SYNC(X, "k_decode");
             ++launches;
         }
-        // k_plan_warp (a warp per item, lane-parallel replay between window
-        // adjustments) beats k_plan (a thread per item) on every measured
-        // population (config 3: 14.13 vs 14.20 ms per evaluation; an evolved
-        // 15.6M-node population: 0.66 vs 0.72 ms); LTGP_PLAN=0 selects k_plan
-        static const int plan_mode = std::getenv("LTGP_PLAN") ? std::atoi(std::getenv("LTGP_PLAN")) : 1;
-        const bool plan_warp = plan_mode != 0;
         if (ni && plan_warp) {  // a warp per item
-            k_plan_warp<<<(ni + 3) / 4, 128, 0, X>>>(s.items.as<Item>() + i0, ni, ts.off.as<uint64_t>(),
-                                                    reinterpret_cast<uint8_t*>(dec), ts.meta.as<uint32_t>(),
-                                                    packets, kWindow, pool);
+            k_plan_warp<true><<<(ni + 3) / 4, 128, 0, X>>>(s.items.as<Item>() + i0, ni, ts.off.as<uint64_t>(),
+                                                          reinterpret_cast<uint8_t*>(dec), ts.meta.as<uint32_t>(),
+                                                          ts.arena.as<uint4>(), packets, kWindow, pool);
             CK(cudaGetLastError());
             DEBUG_SYNC(X, "k_plan_warp");
             ++launches;
