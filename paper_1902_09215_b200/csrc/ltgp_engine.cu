@@ -583,10 +583,15 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         // adjustments) beats k_plan (a thread per item) on every measured
         // population (config 3: 14.13 vs 14.20 ms per evaluation; an evolved
         // 15.6M-node population: 0.66 vs 0.72 ms); LTGP_PLAN=0 selects k_plan.
-        // k_plan_warp also decodes the packets it plans (no k_decode pass).
+        // On a resident evaluation k_plan_warp also decodes the packets it
+        // plans (no k_decode pass: config 3 0.86 -> 0.64 ms). A streamed
+        // slice keeps the separate, fully parallel k_decode: the fused pass
+        // holds SMs longer while earlier slices' k_eval CTAs still occupy the
+        // rest (e2e 2.37 -> 2.14 T GPops/s when fused).
         static const int plan_mode = std::getenv("LTGP_PLAN") ? std::atoi(std::getenv("LTGP_PLAN")) : 1;
         const bool plan_warp = plan_mode != 0;
-        if (p_hi > p_lo && !plan_warp) {
+        const bool fuse_decode = plan_warp && !streamed;
+        if (p_hi > p_lo && !fuse_decode) {
             const uint64_t blocks = std::min<uint64_t>((p_hi - p_lo + 255) / 256, (uint64_t)s.sms * 16);
             k_decode<<<(unsigned)blocks, 256, 0, X>>>(ts.arena.as<uint4>(), dec, ts.meta.as<uint32_t>(), packets,
                                                      p_lo, p_hi);
@@ -594,10 +599,17 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             DEBUG_SYNC(X, "k_decode");
             ++launches;
         }
-        if (ni && plan_warp) {  // a warp per item
+        if (ni && fuse_decode) {  // a warp per item, decoding as it plans
             k_plan_warp<true><<<(ni + 3) / 4, 128, 0, X>>>(s.items.as<Item>() + i0, ni, ts.off.as<uint64_t>(),
                                                           reinterpret_cast<uint8_t*>(dec), ts.meta.as<uint32_t>(),
                                                           ts.arena.as<uint4>(), packets, kWindow, pool);
+            CK(cudaGetLastError());
+            DEBUG_SYNC(X, "k_plan_warp");
+            ++launches;
+        } else if (ni && plan_warp) {  // a warp per item, after k_decode
+            k_plan_warp<false><<<(ni + 3) / 4, 128, 0, X>>>(s.items.as<Item>() + i0, ni, ts.off.as<uint64_t>(),
+                                                           reinterpret_cast<uint8_t*>(dec), ts.meta.as<uint32_t>(),
+                                                           ts.arena.as<uint4>(), packets, kWindow, pool);
             CK(cudaGetLastError());
             DEBUG_SYNC(X, "k_plan_warp");
             ++launches;
