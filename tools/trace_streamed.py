@@ -8,6 +8,9 @@ import torch  # noqa: E402
 
 import paper_1902_09215_b200 as ltgp  # noqa: E402
 
+if os.environ.get("LTGP_CUDA_LIB"):  # a variant from tools/build_variant.py
+    ltgp.CUDA_LIB_PATH = os.environ["LTGP_CUDA_LIB"]
+
 chunk = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 buf, offs, sizes = ltgp.corpus(1, 4000, 4.0, 6.0)
 hb = torch.from_numpy(buf).pin_memory().numpy()
