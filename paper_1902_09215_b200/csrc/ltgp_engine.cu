@@ -449,6 +449,23 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
                 const uint32_t n = ts.h_size[t];
                 if (n <= Cg) all[bstart[32 - __builtin_clz(n)]++] = Item{t, kWholeTree, 0, n};
             }
+            // Resident evaluations of at most 8 waves of the persistent grid
+            // take the items longest first (log2 buckets, stable), so the last
+            // wave is made of the shortest items: evolved populations -2 to
+            // -4% per evaluation. With more waves (config 3: 11) chunks in
+            // tree order measured 2% faster, so they keep it.
+            const uint32_t a0 = s.slice_items[g], a1 = (uint32_t)all.size();
+            const uint64_t grid_warps = (uint64_t)std::max(s.eval_grid, 1) * kWarps;
+            if (G == 1 && (uint64_t)(a1 - a0) <= 8 * grid_warps) {
+                uint32_t cnt[33] = {};
+                for (uint32_t q = a0; q < a1; ++q) ++cnt[32 - __builtin_clz(all[q].hi - all[q].lo)];
+                uint32_t st[33];
+                uint32_t ps = 0;
+                for (int b = 32; b >= 0; --b) { st[b] = ps; ps += cnt[b]; }
+                std::vector<Item> tmp(a1 - a0);
+                for (uint32_t q = a0; q < a1; ++q) tmp[st[32 - __builtin_clz(all[q].hi - all[q].lo)]++] = all[q];
+                std::copy(tmp.begin(), tmp.end(), all.begin() + a0);
+            }
         }
         s.slice_items[G] = (uint32_t)all.size();
         s.slice_ct[G] = (uint32_t)ctrees.size();
