@@ -126,9 +126,13 @@ struct HostBuf {  // grow-only pinned host buffer
     size_t bytes = 0;
     int ensure(size_t need) {
         if (need <= bytes && p) return 0;
+        const size_t old = bytes;
         if (p) cudaFreeHost(p);
         p = nullptr;
-        size_t nb = std::max<size_t>(need, 256);
+        // geometric growth: per-generation work lists fluctuate in size, and
+        // cudaFreeHost + cudaMallocHost costs ~100 us of host time that the
+        // GPU would wait for
+        size_t nb = std::max<size_t>({need + need / 4, 2 * old, size_t(256)});
         if (cudaMallocHost(&p, nb) != cudaSuccess) {
             set_err("cudaMallocHost(%zu) failed", nb);
             p = nullptr;
@@ -206,6 +210,8 @@ struct Shard {
     int sms = 0;
     int eval_grid = 0;
     uint32_t first = 0, count = 0;  // global slot range
+    std::vector<Item> wl_items;                  // work-list scratch (host)
+    std::vector<CombineTree> wl_ctrees;
     bool kev_valid = false;         // kev bracket the last evaluation's k_eval
     TreeSet set[2];
     int cur = 0;
@@ -347,6 +353,7 @@ int launch_combine(ltgp_engine* e, Shard& s, const CombineArgs& ca, cudaStream_t
 // slices' tails free. The upload overlaps the evaluation. Without slices the
 // arena is resident and the whole set is one slice on s.st.
 int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
+    Trace tr;
     CK(cudaSetDevice(s.dev));
     const bool streamed = !s.slices.empty();
     const uint32_t G = streamed ? (uint32_t)s.slices.size() : 1u;
@@ -404,12 +411,17 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         // the per-chunk capacities of the first overflow re-run tier (x4).
         // A chunk's spine and frames grow like sqrt(C) (Remy-random trees:
         // mean ~1.6 sqrt(C), max ~3.6 sqrt(C) frames, ~6 sqrt(C) steps)
+        tr.mark("   chunk len");
         const uint32_t rc = (uint32_t)std::lround(std::sqrt((double)C));
         s.cur_chunk = C;
         s.cur_max_frames = std::max<uint32_t>(kMaxFrames, (6 * rc + 63) & ~63u);
         s.cur_max_steps = std::min<uint32_t>(C, std::max<uint32_t>(kMaxSteps, 16 * rc));
-        std::vector<Item> all;
-        std::vector<CombineTree> ctrees;
+        // host vectors reused across evaluations (capacity kept: fresh
+        // allocations page-faulted ~100 us per generation on evolved runs)
+        std::vector<Item>& all = s.wl_items;
+        std::vector<CombineTree>& ctrees = s.wl_ctrees;
+        all.clear();
+        ctrees.clear();
         s.slice_items.assign(G + 1, 0);
         s.slice_ct.assign(G + 1, 0);
         s.slice_ch.assign(G + 1, 0);
@@ -423,50 +435,61 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             // the final copy: shorter chunks shorten that tail (an item's
             // latency is ~C / 13e6 s)
             const uint32_t Cg = (G > 1 && g == G - 1) ? std::max<uint32_t>(1024, C / 4) : C;
-            // whole trees largest first for load balance: by log2(size)
-            // buckets, descending (linear; stable within a bucket)
-            uint32_t bcount[33] = {};
+            // Item order. Whole trees come largest first for load balance (by
+            // log2(size) buckets, descending; tree order within a bucket),
+            // after the chunks in tree order. Resident evaluations of at most
+            // 8 waves of the persistent grid take all items longest first
+            // (chunks before whole trees within a bucket), so the last wave is
+            // made of the shortest items: evolved populations -2 to -5% per
+            // evaluation. With more waves (config 3: 11) chunks in tree order
+            // measured 2% faster, so they keep it. Two linear passes place
+            // every item directly (no push_back, no sort).
+            auto bucket = [](uint32_t n) { return 32 - __builtin_clz(n); };
+            uint32_t wcnt[33] = {}, ccnt[33] = {};
+            uint32_t nct_g = 0, nch_g = 0;
+            for (uint32_t t = tb[g]; t < tb[g + 1]; ++t) {
+                const uint32_t n = ts.h_size[t];
+                if (n <= Cg) { ++wcnt[bucket(n)]; continue; }
+                const uint32_t k = (n + Cg - 1) / Cg;
+                ++nct_g;
+                nch_g += k;
+                max_chunks = std::max(max_chunks, k);
+                ccnt[bucket(Cg)] += k - 1;
+                ++ccnt[bucket(n - (k - 1) * Cg)];
+            }
+            const uint32_t a0 = (uint32_t)all.size();
+            uint32_t nitems_g = nch_g;
+            for (int b = 0; b <= 32; ++b) nitems_g += wcnt[b];
+            const uint64_t grid_warps = (uint64_t)std::max(s.eval_grid, 1) * kWarps;
+            const bool lpt = G == 1 && (uint64_t)nitems_g <= 8 * grid_warps;
+            uint32_t cpos[33], wpos[33];
+            uint32_t pos = a0, ccur = a0;
+            if (lpt) {
+                for (int b = 32; b >= 0; --b) { cpos[b] = pos; pos += ccnt[b]; wpos[b] = pos; pos += wcnt[b]; }
+            } else {
+                pos += nch_g;
+                for (int b = 32; b >= 0; --b) { wpos[b] = pos; pos += wcnt[b]; }
+            }
+            all.resize(a0 + nitems_g);
+            const uint32_t c0 = (uint32_t)ctrees.size();
+            ctrees.resize(c0 + nct_g);
+            uint32_t ci = c0;
             for (uint32_t t = tb[g]; t < tb[g + 1]; ++t) {
                 const uint32_t n = ts.h_size[t];
                 if (n <= Cg) {
-                    ++bcount[32 - __builtin_clz(n)];
+                    all[wpos[bucket(n)]++] = Item{t, kWholeTree, 0, n};
                     continue;
                 }
                 const uint32_t k = (n + Cg - 1) / Cg;
-                ctrees.push_back({t, nch, k, n});
-                max_chunks = std::max(max_chunks, k);
-                for (uint32_t j = 0; j < k; ++j) all.push_back({t, nch + j, j * Cg, std::min(n, (j + 1) * Cg)});
+                ctrees[ci++] = CombineTree{t, nch, k, n};
+                for (uint32_t q = 0; q < k; ++q) {
+                    const uint32_t lo = q * Cg, hi = std::min(n, lo + Cg);
+                    all[lpt ? cpos[bucket(hi - lo)]++ : ccur++] = Item{t, nch + q, lo, hi};
+                }
                 nch += k;
             }
-            uint32_t bstart[33];
-            uint32_t pos = (uint32_t)all.size();
-            for (int b = 32; b >= 0; --b) {
-                bstart[b] = pos;
-                pos += bcount[b];
-            }
-            all.resize(pos);
-            for (uint32_t t = tb[g]; t < tb[g + 1]; ++t) {
-                const uint32_t n = ts.h_size[t];
-                if (n <= Cg) all[bstart[32 - __builtin_clz(n)]++] = Item{t, kWholeTree, 0, n};
-            }
-            // Resident evaluations of at most 8 waves of the persistent grid
-            // take the items longest first (log2 buckets, stable), so the last
-            // wave is made of the shortest items: evolved populations -2 to
-            // -4% per evaluation. With more waves (config 3: 11) chunks in
-            // tree order measured 2% faster, so they keep it.
-            const uint32_t a0 = s.slice_items[g], a1 = (uint32_t)all.size();
-            const uint64_t grid_warps = (uint64_t)std::max(s.eval_grid, 1) * kWarps;
-            if (G == 1 && (uint64_t)(a1 - a0) <= 8 * grid_warps) {
-                uint32_t cnt[33] = {};
-                for (uint32_t q = a0; q < a1; ++q) ++cnt[32 - __builtin_clz(all[q].hi - all[q].lo)];
-                uint32_t st[33];
-                uint32_t ps = 0;
-                for (int b = 32; b >= 0; --b) { st[b] = ps; ps += cnt[b]; }
-                std::vector<Item> tmp(a1 - a0);
-                for (uint32_t q = a0; q < a1; ++q) tmp[st[32 - __builtin_clz(all[q].hi - all[q].lo)]++] = all[q];
-                std::copy(tmp.begin(), tmp.end(), all.begin() + a0);
-            }
         }
+        tr.mark("   items");
         s.slice_items[G] = (uint32_t)all.size();
         s.slice_ct[G] = (uint32_t)ctrees.size();
         s.slice_ch[G] = nch;
@@ -474,6 +497,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         // the pinned staging buffers are reused: wait for their last copies
         // (not for the whole stream: a splice may still be running)
         CK(cudaEventSynchronize(s.ev[7]));
+        tr.mark("   ev7 wait");
         TRY(s.h_items.ensure(sizeof(Item) * std::max<uint32_t>(nitems, 1)));
         std::copy(all.begin(), all.end(), s.h_items.as<Item>());
         TRY(s.items.ensure(sizeof(Item) * std::max<uint32_t>(nitems, 1), s.dev));
@@ -492,6 +516,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             TRY(s.cch.ensure(sizeof(CombChunk) * nch, s.dev));
             TRY(s.cres.ensure(sizeof(CombResult) * nct, s.dev));
         }
+        tr.mark("  work list");
         s.last_items = nitems;
         s.last_chunks = nch;
         s.last_ctrees = nct;
@@ -575,6 +600,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     a.packets = packets;
     if (streamed)
         for (int k = 1; k < kComputeStreams && k < (int)G; ++k) TRY(s.xspill[k].ensure(s.spill.bytes, s.dev));
+    tr.mark("  pool/setup");
     CK(cudaEventRecord(s.ev[0], s.st));
     s.kev_valid = false;
     uint32_t launches = 0;
@@ -676,6 +702,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     CK(cudaEventRecord(s.ev[1], s.st));
     CK(cudaMemcpyAsync(s.h_counters.p, s.counters.p, 64, cudaMemcpyDeviceToHost, s.st));
     e->stats.kernel_launches = launches;
+    tr.mark("  launches");
     return 0;
 }
 
