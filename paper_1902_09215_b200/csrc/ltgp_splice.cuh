@@ -47,12 +47,20 @@ __global__ void __launch_bounds__(128) k_extent(const PlanDev* plans, uint32_t c
     uint64_t base = pt & ~uint64_t(15);
     uint64_t end = 0;
     bool found = false;
+    // the next 512-byte block is loaded while this one is scanned (long
+    // subtrees of deep evolved trees take hundreds of dependent steps)
+    auto load = [&](uint64_t b) {
+        const uint64_t l = b + 16ull * lane;
+        return l < n ? *reinterpret_cast<const uint4*>(d.ptr + l) : make_uint4(0u, 0u, 0u, 0u);
+    };
+    uint4 wnext = load(base);
     while (!found && base < n) {
         const uint64_t lb = base + 16ull * lane;  // this lane's 16 bytes
+        const uint4 w = wnext;
+        wnext = load(base + 512);
         int delta[16];
         int tot = 0;
         if (lb < n) {
-            const uint4 w = *reinterpret_cast<const uint4*>(d.ptr + lb);
             const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
