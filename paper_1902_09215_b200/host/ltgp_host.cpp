@@ -166,30 +166,44 @@ void validate(const RunConfig& c) {
     if (c.tournament_size < 1) throw std::invalid_argument("tournament_size < 1");
 }
 
-// evolve.hpp:79-82 (SURVEY.md App. A #7)
-std::size_t tournament(Rng& rng, std::span<const Individual> pop, std::uint32_t k) {
-    const std::uint64_t M = pop.size();
+namespace {
+// evolve.hpp:79-82 over any fitness accessor: the
+// reference's draws and comparisons
+template <class Fit>
+std::size_t tournament_by(Rng& rng, std::uint64_t M, std::uint32_t k, Fit fit) {
     std::size_t best = static_cast<std::size_t>(rng.below(M));
     std::uint64_t ties = 1;
     for (std::uint32_t i = 1; i < k; ++i) {
         const std::size_t idx = static_cast<std::size_t>(rng.below(M));
-        if (fitness_better(pop[idx].fitness, pop[best].fitness)) {
+        if (fitness_better(fit(idx), fit(best))) {
             best = idx;
             ties = 1;
-        } else if (fitness_tied(pop[idx].fitness, pop[best].fitness)) {
+        } else if (fitness_tied(fit(idx), fit(best))) {
             if (rng.below(ties + 1) == 0) best = idx;
             ++ties;
         }
     }
     return best;
 }
+}  // namespace
 
-// evolve.hpp:84-87
+// evolve.hpp:79-82 (SURVEY.md App. A #7)
+std::size_t tournament(Rng& rng, std::span<const Individual> pop, std::uint32_t k) {
+    return tournament_by(rng, pop.size(), k, [&](std::size_t i) { return pop[i].fitness; });
+}
+
+// evolve.hpp:84-87. The tournaments read fitness from a
+// dense copy (4 B per individual, L1-resident) instead of the 40-byte
+// Individuals; the draws and comparisons are unchanged.
 std::vector<CrossoverPlan> plan_generation(Rng& rng, std::span<const Individual> pop, std::uint32_t k) {
+    std::vector<float> fit(pop.size());
+    for (std::size_t i = 0; i < pop.size(); ++i) fit[i] = pop[i].fitness;
+    const float* f = fit.data();
+    auto dense = [f](std::size_t i) { return f[i]; };
     std::vector<CrossoverPlan> plans(pop.size());
     for (auto& p : plans) {
-        p.mum_index = static_cast<std::uint32_t>(tournament(rng, pop, k));
-        p.dad_index = static_cast<std::uint32_t>(tournament(rng, pop, k));
+        p.mum_index = static_cast<std::uint32_t>(tournament_by(rng, pop.size(), k, dense));
+        p.dad_index = static_cast<std::uint32_t>(tournament_by(rng, pop.size(), k, dense));
         p.mum_pt = static_cast<std::uint32_t>(rng.below(pop[p.mum_index].size));
         p.dad_pt = static_cast<std::uint32_t>(rng.below(pop[p.dad_index].size));
     }
