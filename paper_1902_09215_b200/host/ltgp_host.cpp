@@ -607,6 +607,7 @@ int64_t ltgp_host_run_checkpointed(ltgp_engine* e, uint32_t M, uint32_t G, uint6
                                    const char* ckpt_path, uint32_t ckpt_every, const char* resume_path,
                                    int* reason, uint64_t* nodes, double* eval_seconds) {
     try {
+        if (!reason || !nodes) throw std::invalid_argument("null reason / nodes_evaluated pointer");
         RunConfig cfg;
         cfg.population_size = M;
         cfg.max_generations = G;

@@ -94,3 +94,11 @@ def test_run_bench_argument_validation_without_gpu():
     for sizes, workers in (([], [1]), ([1001], []), ([1001], [0]), ([1001], [17])):
         with pytest.raises(ltgp.EngineError):
             ltgp.run_bench(sizes, workers, min_corpus_nodes=1000, repeats=1)
+
+
+def test_run_null_out_pointers_are_errors():
+    """The C ABI reports null out-pointers as an error instead of crashing."""
+    import ctypes as C
+    lib = ltgp.host_lib()
+    assert lib.ltgp_host_run_checkpointed(None, 48, 10, 10**9, 7, 1, 1, 0, None, None, 0, None,
+                                          None, None, None) == -1
