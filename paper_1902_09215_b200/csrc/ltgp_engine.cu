@@ -398,7 +398,13 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             };
             const uint64_t k0 = chunks_of(C);
             const uint64_t waves = (k0 + W - 1) / W;
-            if (k0 > W / 2 && waves <= 8 && C >= 2048) {
+            // Only for a few huge trees (config 4's regime): with thousands of
+            // chunked trees (an evolved generation 3000: 3000+) the shorter
+            // chunks cost more than the fuller last wave gains (4.33 vs 4.62
+            // ms per evaluation without the rule there).
+            uint64_t big_trees = 0;  // trees that get chunked
+            for (uint32_t t = 0; t < ts.count; ++t) big_trees += ts.h_size[t] > C;
+            if (k0 > W / 2 && waves <= 8 && C >= 2048 && big_trees <= 512) {
                 uint32_t lo = std::max<uint32_t>(1024, C / 2) / 1024, hi = C / 1024;  // in units of 1024
                 while (lo < hi) {  // smallest c with chunks_of(c) <= waves * W (non-increasing in c)
                     const uint32_t mid = (lo + hi) / 2;

@@ -9,7 +9,7 @@ if os.environ.get("LTGP_CUDA_LIB"):  # a variant from tools/build_variant.py
     ltgp.CUDA_LIB_PATH = os.environ["LTGP_CUDA_LIB"]
 
 G = int(sys.argv[1]) if len(sys.argv) > 1 else 200
-with ltgp.Engine([0], node_limit=2**62) as e:
+with ltgp.Engine([0], node_limit=2**62, chunk_nodes=int(os.environ.get("LTGP_CHUNK", "0"))) as e:
     e.run(4000, G, 2**62, 7, 1, None, 1)
     for _ in range(3):
         rec = e.evaluate_population()
