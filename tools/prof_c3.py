@@ -15,7 +15,7 @@ def main():
     reps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
     trees = int(sys.argv[2]) if len(sys.argv) > 2 else 4000
     buf, offs, sizes = ltgp.corpus(1, trees, 4.0, 6.0)
-    with ltgp.Engine([0]) as e:
+    with ltgp.Engine([0], chunk_nodes=int(os.environ.get("LTGP_CHUNK", "0"))) as e:
         e.set_suite(*ltgp.make_suite(ltgp.suite_seed(1)))
         e.upload_packed(buf, offs, sizes)
         for _ in range(reps):
