@@ -1540,7 +1540,11 @@ int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M, 
                                                               s.dir.as<DirEntry>(), s.ext.as<Extent>(),
                                                               s.csize.as<uint64_t>());
         CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(ext.data() + qfirst[g], s.ext.p, sizeof(Extent) * qcount[g], cudaMemcpyDeviceToHost, s.st));
+        // one shard splices exactly the children whose extents it computed:
+        // the extents and plans stay on the device (no round trip)
+        if (G > 1)
+            CK(cudaMemcpyAsync(ext.data() + qfirst[g], s.ext.p, sizeof(Extent) * qcount[g], cudaMemcpyDeviceToHost,
+                               s.st));
         CK(cudaMemcpyAsync(csize.data() + qfirst[g], s.csize.p, sizeof(uint64_t) * qcount[g], cudaMemcpyDeviceToHost, s.st));
         CK(cudaMemcpyAsync(s.h_counters.p, s.counters.p, 64, cudaMemcpyDeviceToHost, s.st));
     }
@@ -1580,12 +1584,17 @@ int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M, 
         uint8_t* hb = s.h_coff.as<uint8_t>();
         std::memcpy(hb, coff.data(), sizeof(uint64_t) * s.count);
         std::memcpy(hb + 8 * s.count, csize.data() + s.first, sizeof(uint64_t) * s.count);
-        std::memcpy(hb + 16 * s.count, ext.data() + s.first, sizeof(Extent) * s.count);
-        std::memcpy(hb + 32 * s.count, plans + s.first, sizeof(PlanDev) * s.count);
+        if (G > 1) {
+            std::memcpy(hb + 16 * s.count, ext.data() + s.first, sizeof(Extent) * s.count);
+            std::memcpy(hb + 32 * s.count, plans + s.first, sizeof(PlanDev) * s.count);
+        }
         CK(cudaMemcpyAsync(s.coff.p, hb, 8 * s.count, cudaMemcpyHostToDevice, s.st));
         CK(cudaMemcpyAsync(s.csize.p, hb + 8 * s.count, 8 * s.count, cudaMemcpyHostToDevice, s.st));
-        CK(cudaMemcpyAsync(s.ext.p, hb + 16 * s.count, sizeof(Extent) * s.count, cudaMemcpyHostToDevice, s.st));
-        CK(cudaMemcpyAsync(s.plans.p, hb + 32 * s.count, sizeof(PlanDev) * s.count, cudaMemcpyHostToDevice, s.st));
+        if (G > 1) {
+            CK(cudaMemcpyAsync(s.ext.p, hb + 16 * s.count, sizeof(Extent) * s.count, cudaMemcpyHostToDevice, s.st));
+            CK(cudaMemcpyAsync(s.plans.p, hb + 32 * s.count, sizeof(PlanDev) * s.count, cudaMemcpyHostToDevice,
+                               s.st));
+        }
         CK(cudaEventRecord(s.ev[2], s.st));
         k_splice<<<std::min<uint32_t>(s.count, (uint32_t)s.sms * 8), 256, 0, s.st>>>(
             s.plans.as<PlanDev>(), s.count, s.dir.as<DirEntry>(), s.ext.as<Extent>(), s.coff.as<uint64_t>(),
