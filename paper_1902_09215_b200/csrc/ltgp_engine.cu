@@ -400,14 +400,22 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
                     if (ts.h_size[t] > c) k += (ts.h_size[t] + c - 1) / c;
                 return k;
             };
-            const uint64_t k0 = chunks_of(C);
+            // chunks at C (C is a power of two here: shifts) and the trees
+            // that get chunked, in one pass
+            uint64_t k0 = 0, big_trees = 0;
+            {
+                const uint32_t sh = (uint32_t)__builtin_ctz(C);
+                for (uint32_t t = 0; t < ts.count; ++t)
+                    if (ts.h_size[t] > C) {
+                        k0 += ((uint64_t)ts.h_size[t] + C - 1) >> sh;
+                        ++big_trees;
+                    }
+            }
             const uint64_t waves = (k0 + W - 1) / W;
             // Only for a few huge trees (config 4's regime): with thousands of
             // chunked trees (an evolved generation 3000: 3000+) the shorter
             // chunks cost more than the fuller last wave gains (4.33 vs 4.62
             // ms per evaluation without the rule there).
-            uint64_t big_trees = 0;  // trees that get chunked
-            for (uint32_t t = 0; t < ts.count; ++t) big_trees += ts.h_size[t] > C;
             if (k0 > W / 2 && waves <= 8 && C >= 2048 && big_trees <= 512) {
                 uint32_t lo = std::max<uint32_t>(1024, C / 2) / 1024, hi = C / 1024;  // in units of 1024
                 while (lo < hi) {  // smallest c with chunks_of(c) <= waves * W (non-increasing in c)
