@@ -97,18 +97,43 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def cpu_info():
+    """CPU model and hardware threads of this host (BASELINE.md's CPU plan)."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"model": model, "nproc": os.cpu_count() or 1}
+
+
+def workload_config(world, sizes_of):
+    """The config dict both arms print (identical keys and values): the
+    config-3 batch per GPU, seeds SEED + r for r < world."""
+    sizes = [sizes_of(SEED + r) for r in range(world)]
+    nodes = sum(int(s.sum()) for s in sizes)
+    return {"workload": "c3", "trees_per_gpu": M_TREES, "lg_nodes": [LG_LO, LG_HI],
+            "seeds": [SEED + r for r in range(world)], "nodes": nodes, "gpops_per_step": nodes * LANES,
+            "parallelism": f"population shards x{world}" + (" + NCCL all-gather of records" if world > 1 else ""),
+            "l2": "inputs larger than L2: %.0f MB of opcodes per GPU vs 126 MB L2" % (int(sizes[0].sum()) / 1e6)}
+
+
 def oracle_sample(threads, seconds_target, first_trees=None):
     """Time the oracle's multi-threaded evaluate_population (the reference's
-    CPU algorithm as restated in oracle/) on a prefix of the workload."""
-    import paper_1902_09215_b200 as ltgp
+    CPU algorithm as restated in oracle/) on a prefix of the workload. Only
+    the oracle library is loaded here: suite and corpus come from its own
+    generators (byte-identical to the product's, tests/test_oracle.py)."""
     from tests._oracle import load_oracle
 
     o = load_oracle()
-    suite = ltgp.make_suite(ltgp.suite_seed(SEED))
-    sizes = ltgp.corpus_sizes(SEED, M_TREES, LG_LO, LG_HI)
+    suite = o.make_suite(int(o.orc_suite_seed(SEED)))
+    sizes = o.corpus_sizes(SEED, M_TREES, LG_LO, LG_HI)
     # calibrate on the first few trees
     n_cal = 8
-    buf, offs, sz = ltgp.corpus(SEED, M_TREES, LG_LO, LG_HI, first=0, n=n_cal)
+    buf, offs, sz = o.corpus(SEED, M_TREES, LG_LO, LG_HI, first=0, n=n_cal)
     t0 = time.perf_counter()
     o.evaluate_population(buf, offs, sz, suite, threads=threads)
     rate = float(sz.sum()) / max(time.perf_counter() - t0, 1e-6)  # nodes/s
@@ -116,13 +141,18 @@ def oracle_sample(threads, seconds_target, first_trees=None):
     if first_trees is None:
         csum = np.cumsum(sizes.astype(np.float64))
         first_trees = int(min(M_TREES, max(n_cal, np.searchsorted(csum, budget) + 1)))
-    buf, offs, sz = ltgp.corpus(SEED, M_TREES, LG_LO, LG_HI, first=0, n=first_trees)
+    buf, offs, sz = o.corpus(SEED, M_TREES, LG_LO, LG_HI, first=0, n=first_trees)
     return o, suite, buf, offs, sz, first_trees
 
 
 def run_reference(args, rank, world):
+    """The reference's CPU path (the oracle port: the reference is a header
+    skeleton without function bodies, so its own evaluator cannot be built)
+    on all host threads, rank 0 only. Never loads the product libraries."""
     if rank != 0:
         return
+    from tests._oracle import load_oracle
+
     threads = os.cpu_count() or 1
     per_step = max(2.0, min(10.0, 150.0 / max(1, args.steps + args.warmup)))
     o, suite, buf, offs, sz, ntrees = oracle_sample(threads, per_step)
@@ -134,16 +164,19 @@ def run_reference(args, rank, world):
         o.evaluate_population(buf, offs, sz, suite, threads=threads)
     dt = time.perf_counter() - t0
     value = nodes * LANES * args.steps / dt
+    cpu = cpu_info()
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "GPops/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GPops/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded config-3 corpus)",
-        "config": {"workload": "c3", "trees": M_TREES, "lg_nodes": [LG_LO, LG_HI], "seed": SEED,
-                   "sample_trees": ntrees, "sample_nodes": nodes},
+        "data": "synthetic (seeded config-3 corpus, generated on the host)",
+        "config": workload_config(world, lambda sd: o.corpus_sizes(sd, M_TREES, LG_LO, LG_HI)),
         "cpu_baseline": {"value": value, "unit": "GPops/s", "cores": threads, "kind": "port",
+                         "cpu": cpu,
                          "sample": f"first {ntrees} of {M_TREES} config-3 trees ({nodes} nodes) per step; "
-                                   f"oracle eval_batch (48-lane AVX frames) on a {threads}-thread dynamic pool"},
+                                   f"oracle eval_batch (48-lane AVX frames, the reference's eval_batch_raw "
+                                   f"restated) on a {threads}-thread dynamic pool; the reference itself is "
+                                   f"declarations only and cannot run"},
         "e2e": {"value": value, "unit": "GPops/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -282,11 +315,7 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded config-3 corpus, generated on the host)",
-        "config": {"workload": "c3", "trees_per_gpu": M_TREES, "lg_nodes": [LG_LO, LG_HI],
-                   "seeds": [SEED + r for r in range(world)],
-                   "nodes": nodes_job, "gpops_per_step": nodes_job * LANES,
-                   "parallelism": f"population shards x{world}" + (" + NCCL all-gather of records" if world > 1 else ""),
-                   "l2": "inputs larger than L2: %.0f MB of opcodes per GPU vs 126 MB L2" % (nodes_rank / 1e6)},
+        "config": workload_config(world, lambda sd: ltgp.corpus_sizes(sd, M_TREES, LG_LO, LG_HI)),
         "e2e": {"value": e2e, "unit": "GPops/s", "h2d_bytes_per_step": bytes_job,
                 "d2h_bytes_per_step": M_TREES * 16 * world},
         "gpu_launches": launches,
@@ -323,7 +352,7 @@ def run_ours(args, rank, world, local_rank):
         o.evaluate_population(cb, co, cs, s2, threads=threads)
         dt = time.perf_counter() - t0
         line["cpu_baseline"] = {"value": float(cs.sum()) * LANES / dt, "unit": "GPops/s", "cores": threads,
-                                "kind": "port",
+                                "kind": "port", "cpu": cpu_info(),
                                 "sample": f"first {ntrees} of {M_TREES} config-3 trees ({int(cs.sum())} nodes); "
                                           f"oracle eval_batch on a {threads}-thread pool, {dt:.1f} s"}
     if rank == 0:

@@ -69,7 +69,7 @@ typedef struct {
     uint64_t last_window_adjusts; /* of which needed a stack window spill or refill */
     uint64_t last_spine_steps;  /* spine steps the chunk summaries of the last evaluation hold */
     uint32_t kernel_launches;   /* engine kernels launched by the last call */
-    uint32_t pad0;
+    uint32_t gather_nccl;       /* 1: records are all-gathered by NCCL (distinct devices, use_nccl) */
     double keval_seconds;       /* k_eval alone, max over shards (resident evaluations; 0 when streamed) */
 } ltgp_stats;
 
@@ -91,6 +91,8 @@ typedef struct {
 } ltgp_gen_stats;
 
 const char* ltgp_last_error(void);
+/* Visible CUDA devices (for callers that map workers to GPUs). */
+int ltgp_device_count(int* n);
 const char* ltgp_version(void);
 
 int ltgp_engine_create(const ltgp_config* cfg, ltgp_engine** out);
@@ -163,6 +165,10 @@ int ltgp_download_genome(ltgp_engine* e, uint32_t idx, uint8_t* buf, uint64_t ca
 
 /* eval_batch (eval.hpp:78-79) of one genome: the 48 per-case outputs. */
 int ltgp_eval_one(ltgp_engine* e, const uint8_t* ops, uint64_t n, float* out48);
+
+/* ltgp_eval_one plus the individual's record (evaluate_individual,
+   evolve.hpp:106: fitness, hits, size, depth computed on the device). */
+int ltgp_eval_one_record(ltgp_engine* e, const uint8_t* ops, uint64_t n, float* out48, ltgp_record* rec);
 
 /* subtree_extent (genome.hpp:56-57) of `count` (slot, point) queries on
    device; out holds [start, end) pairs. */

@@ -509,6 +509,47 @@ int orc_random_tree_of_size(uint64_t seed, uint64_t n, uint8_t* out) {
     Rng r(seed);
     return random_tree_of_size(r, n, out) ? 0 : -1;
 }
+// The config-3 evaluation corpus (BASELINE.json configs[2]), restated here so
+// that bench.py's reference arm builds its workload without loading any
+// product library: sizes odd(floor(10^(lo + (hi-lo) u))), u from the top 53
+// bits of Rng(seed).below(2^53); tree i from Rng(tree_seed(seed, i)) by
+// random_tree_of_size (bench.hpp:13-15); each tree 16-byte aligned and padded
+// with 0xFF. Same layout as the product's generator (test_oracle.py checks
+// the bytes are identical).
+static uint64_t tree_seed(uint64_t seed, uint32_t i) {
+    return splitmix64(seed ^ (0x7265657274ull + (uint64_t)i * 0x9e3779b97f4a7c15ull));
+}
+uint64_t orc_corpus(uint64_t seed, uint32_t M, double lg_lo, double lg_hi, uint32_t first, uint32_t count,
+                    uint8_t* buf, uint64_t* offsets, uint64_t* sizes, int threads) {
+    Rng rng(seed);
+    for (uint32_t i = 0; i < M; ++i) {
+        const double u = static_cast<double>(rng.below(1ull << 53)) * 0x1.0p-53;
+        const uint64_t n = static_cast<uint64_t>(std::floor(std::pow(10.0, lg_lo + (lg_hi - lg_lo) * u)));
+        sizes[i] = n | 1u;
+    }
+    if (first > M) first = M;
+    if (count > M - first) count = M - first;
+    uint64_t total = 0;
+    for (uint32_t j = 0; j < count; ++j) {
+        if (offsets) offsets[j] = total;
+        total += (sizes[first + j] + 15) & ~uint64_t(15);
+    }
+    if (!buf || !offsets) return total;
+    if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+    std::atomic<uint32_t> next{0};
+    auto work = [&]() {
+        for (uint32_t j; (j = next.fetch_add(1)) < count;) {
+            const uint32_t i = first + j;
+            Rng r(tree_seed(seed, i));
+            random_tree_of_size(r, sizes[i], buf + offsets[j]);
+            std::memset(buf + offsets[j] + sizes[i], 0xff, ((sizes[i] + 15) & ~uint64_t(15)) - sizes[i]);
+        }
+    };
+    std::vector<std::thread> ts;
+    for (int t = 0; t < threads; ++t) ts.emplace_back(work);
+    for (auto& t : ts) t.join();
+    return total;
+}
 float orc_eval_scalar(const uint8_t* ops, uint64_t n, float x, const float* cs) {
     return eval_scalar(ops, n, x, cs);
 }

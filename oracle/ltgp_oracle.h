@@ -68,6 +68,11 @@ uint64_t orc_ramped_half_and_half(uint64_t seed, uint32_t count, uint64_t capaci
                                   int max_depth, uint8_t* out, uint64_t out_cap, uint64_t* sizes);
 /* random_tree_of_size from Rng(seed) (one tree per call). */
 int orc_random_tree_of_size(uint64_t seed, uint64_t n, uint8_t* out);
+/* BASELINE.json configs[2] corpus (same bytes as the product's generator):
+   sizes[M] always; with buf/offsets, trees [first, first+count) packed
+   16-byte aligned. Returns the packed byte count. */
+uint64_t orc_corpus(uint64_t seed, uint32_t M, double lg_lo, double lg_hi, uint32_t first, uint32_t count,
+                    uint8_t* buf, uint64_t* offsets, uint64_t* sizes, int threads);
 /* eval.hpp:65-87 */
 float orc_eval_scalar(const uint8_t* ops, uint64_t n, float x, const float* consts250);
 /* 0 ok, <0 malformed; out48 receives the result frame; peak receives peak frames */

@@ -56,7 +56,7 @@ class _Stats(C.Structure):
                 ("arena_high_water", C.c_uint64), ("last_chunks", C.c_uint64),
                 ("last_fallback_items", C.c_uint64), ("last_exits", C.c_uint64),
                 ("last_window_adjusts", C.c_uint64), ("last_spine_steps", C.c_uint64),
-                ("kernel_launches", C.c_uint32), ("pad0", C.c_uint32), ("keval_seconds", C.c_double)]
+                ("kernel_launches", C.c_uint32), ("gather_nccl", C.c_uint32), ("keval_seconds", C.c_double)]
 
 
 _cuda = None
@@ -67,6 +67,7 @@ _P = C.c_void_p
 _CUDA_SIGS = {
     "ltgp_last_error": (C.c_char_p, []),
     "ltgp_version": (C.c_char_p, []),
+    "ltgp_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "ltgp_engine_create": (C.c_int, [C.POINTER(_Config), C.POINTER(_P)]),
     "ltgp_engine_destroy": (C.c_int, [_P]),
     "ltgp_set_suite": (C.c_int, [_P, _P, _P, _P]),
@@ -82,6 +83,7 @@ _CUDA_SIGS = {
     "ltgp_execute_generation": (C.c_int, [_P, _P, C.c_uint32, _P, C.POINTER(C.c_int)]),
     "ltgp_download_genome": (C.c_int, [_P, C.c_uint32, _P, C.c_uint64, C.POINTER(C.c_uint64)]),
     "ltgp_eval_one": (C.c_int, [_P, _P, C.c_uint64, _P]),
+    "ltgp_eval_one_record": (C.c_int, [_P, _P, C.c_uint64, _P, _P]),
     "ltgp_subtree_extents": (C.c_int, [_P, C.c_uint32, _P, _P, _P]),
     "ltgp_get_stats": (C.c_int, [_P, C.POINTER(_Stats)]),
     "ltgp_population_size": (C.c_uint32, [_P]),
@@ -401,6 +403,14 @@ class Engine:
         st = _Stats()
         _check(self._lib.ltgp_get_stats(self._h, C.byref(st)))
         return {k: getattr(st, k) for k, _ in _Stats._fields_}
+
+    def gather_mode(self) -> str:
+        """How multi-shard records are all-gathered: "nccl" (distinct devices,
+        one grouped ncclAllGather), "copies" (peer copies to shard 0: shards
+        that repeat a device) or "none" (one shard)."""
+        if self.stats()["gather_nccl"]:
+            return "nccl"
+        return "copies" if len(self.devices) > 1 else "none"
 
     def shard_records(self, s: int):
         p, f, n, st = _P(), C.c_uint32(), C.c_uint32(), _P()

@@ -70,8 +70,38 @@ def build(force: bool = False, verbose: bool = False) -> None:
     if force or _stale(HOST_LIB, host_deps):
         _run(["g++", *CXX_FLAGS, "-shared", "-o", HOST_LIB, os.path.join(HOST, "ltgp_host.cpp"),
               "-L" + PKG, "-lltgp_cuda", "-Wl,-rpath,$ORIGIN"])
+    build_refabi(force)
     if verbose:
         print("built", CUDA_LIB, HOST_LIB)
+
+
+REF_INC = "/root/reference/proj/include"
+REFABI_LIB = os.path.join(PKG, "libltgp_refabi.so")
+REFABI_SRC = os.path.join(HOST, "evolve_cuda.cpp")
+REF_RUN_SRC = os.path.join(ROOT, "tests", "refabi", "ref_run.cpp")
+REF_RUN_BIN = os.path.join(ROOT, "tests", "refabi", "_bin", "ref_run")
+
+
+def build_refabi(force: bool = False) -> bool:
+    """libltgp_refabi.so: the reference-typed drop-in (evolve_cuda.cpp),
+    compiled against the reference's unmodified headers where they lie, plus
+    the reference-typed test harness tests/refabi/_bin/ref_run. Built only
+    when /root/reference is present (this container); the built files travel
+    to the GPU box like the other .so files. Returns whether they exist."""
+    if not os.path.isdir(REF_INC):
+        return os.path.exists(REFABI_LIB)
+    inc = ["-I" + REF_INC, "-I" + os.path.join(ROOT, "include")]
+    deps = [REFABI_SRC, os.path.join(ROOT, "include", "ltgp_refabi.h"), CUDA_LIB]
+    if force or _stale(REFABI_LIB, deps):
+        _run(["g++", *CXX_FLAGS, *inc, "-shared", "-o", REFABI_LIB, REFABI_SRC,
+              "-L" + PKG, "-lltgp_cuda", "-Wl,-rpath,$ORIGIN"])
+    oracle_lib = os.path.join(ROOT, "oracle", "libltgp_oracle.so")
+    if os.path.exists(oracle_lib) and (force or _stale(REF_RUN_BIN, [REF_RUN_SRC, REFABI_LIB, oracle_lib])):
+        os.makedirs(os.path.dirname(REF_RUN_BIN), exist_ok=True)
+        _run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-Wall", *inc, "-o", REF_RUN_BIN, REF_RUN_SRC,
+              "-L" + PKG, "-lltgp_refabi", "-lltgp_cuda", "-L" + os.path.dirname(oracle_lib), "-lltgp_oracle",
+              "-Wl,-rpath,$ORIGIN/../../../paper_1902_09215_b200:$ORIGIN/../../../oracle"])
+    return True
 
 
 if __name__ == "__main__":

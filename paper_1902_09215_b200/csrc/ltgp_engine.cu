@@ -8,6 +8,7 @@
 
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 #include <nccl.h>  // types only: libnccl is opened at run time (see RecordGather)
 
 #include <algorithm>
@@ -41,11 +42,26 @@ constexpr int kRerunCtas = 8;
 
 thread_local std::string g_err;
 
-// LTGP_TRACE=1: per-phase host wall times of execute_generation on stderr.
+// NVTX3 ranges (header-only; no-ops unless a tool such as nsys attaches):
+// one range per engine phase (work list / plan / k_eval / combine / extents /
+// splice / gather), so a timeline shows the host orchestration around the
+// kernels.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
+// LTGP_TRACE=1: per-phase host wall times of execute_generation on stderr;
+// every mark is also an NVTX marker, and the Trace's lifetime an NVTX range.
 struct Trace {
     bool on = std::getenv("LTGP_TRACE") != nullptr;
     std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    explicit Trace(const char* name) { nvtxRangePushA(name); }
+    ~Trace() { nvtxRangePop(); }
     void mark(const char* what) {
+        nvtxMarkA(what);
         if (!on) return;
         const auto t = std::chrono::steady_clock::now();
         std::fprintf(stderr, "[ltgp] %-12s %8.1f us\n", what,
@@ -353,7 +369,7 @@ int launch_combine(ltgp_engine* e, Shard& s, const CombineArgs& ca, cudaStream_t
 // slices' tails free. The upload overlaps the evaluation. Without slices the
 // arena is resident and the whole set is one slice on s.st.
 int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
-    Trace tr;
+    Trace tr("ltgp.evaluate");
     CK(cudaSetDevice(s.dev));
     const bool streamed = !s.slices.empty();
     const uint32_t G = streamed ? (uint32_t)s.slices.size() : 1u;
@@ -452,7 +468,9 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             // the last slice of a streamed evaluation is all that runs after
             // the final copy: shorter chunks shorten that tail (an item's
             // latency is ~C / 13e6 s)
-            const uint32_t Cg = (G > 1 && g == G - 1) ? std::max<uint32_t>(1024, C / 4) : C;
+            // (never longer than C: the re-run tiers size worst-case
+            // capacities from C)
+            const uint32_t Cg = (G > 1 && g == G - 1) ? std::min<uint32_t>(C, std::max<uint32_t>(1024, C / 4)) : C;
             // Item order. Whole trees come largest first for load balance (by
             // log2(size) buckets, descending; tree order within a bucket),
             // after the chunks in tree order. Resident evaluations of at most
@@ -570,6 +588,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     }
     pool.spill_frames = spill_frames(s.cur_chunk);
     pool.adjusts = s.counters.as<uint32_t>() + 5;  // inline window adjusts join the statistics
+    pool.flags = s.counters.as<uint32_t>() + 1;    // opcode 255 inside a tree: malformed
     TRY(s.rec.ensure(sizeof(ltgp_record) * std::max<uint32_t>(ts.count, 1), s.dev));
     if (want_outs) TRY(s.outs.ensure(sizeof(float) * kLanes * std::max<uint32_t>(ts.count, 1), s.dev));
     CK(cudaMemsetAsync(s.counters.p, 0, kCounterBytes, s.st));
@@ -657,6 +676,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         static const int plan_mode = std::getenv("LTGP_PLAN") ? std::atoi(std::getenv("LTGP_PLAN")) : 1;
         const bool plan_warp = plan_mode != 0;
         const bool fuse_decode = plan_warp && !streamed;
+        NvtxRange nr_plan("ltgp.decode+plan");
         if (p_hi > p_lo && !fuse_decode) {
             const uint64_t blocks = std::min<uint64_t>((p_hi - p_lo + 255) / 256, (uint64_t)s.sms * 16);
             k_decode<<<(unsigned)blocks, 256, 0, X>>>(ts.arena.as<uint4>(), dec, ts.meta.as<uint32_t>(), packets,
@@ -741,6 +761,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
 // and chunks `ca` names, on stream st.
 int launch_combine(ltgp_engine* e, Shard& s, const CombineArgs& ca, cudaStream_t st, uint32_t& launches) {
     if (ca.n_trees == 0) return 0;
+    NvtxRange nr("ltgp.spine_combine");
     // k_cpops's segment stack in shared memory: 2 per chunk of the tree
     const uint32_t segs = std::min<uint32_t>(2 * s.max_tree_chunks, kCpopsSmem / (uint32_t)sizeof(Seg));
     k_cpops<<<ca.n_trees, 32, segs * sizeof(Seg), st>>>(ca, segs);
@@ -759,6 +780,7 @@ int launch_combine(ltgp_engine* e, Shard& s, const CombineArgs& ca, cudaStream_t
 }
 
 int rerun_overflowed(ltgp_engine* e, Shard& s) {
+    NvtxRange nr("ltgp.overflow_rerun");
     CK(cudaSetDevice(s.dev));
     const uint32_t C = s.cur_chunk;
     std::vector<Item> prev(s.h_items.as<Item>(), s.h_items.as<Item>() + s.last_items);
@@ -857,8 +879,9 @@ int check_eval(Shard& s) {
         return -1;
     }
     if (flags & 8u) { set_err("k_eval shared-memory layout does not fit"); return -1; }
+    // malformed first: an invalid genome also derails the plan/scan cross-check
+    if (flags & 2u) { set_err("malformed genome (stack underflow, leftover values or opcode 255 inside a tree)"); return -1; }
     if (flags & 16u) { set_err("chunk summary differs from k_plan's sizing (internal error)"); return -1; }
-    if (flags & 2u) { set_err("malformed genome (stack underflow or leftover values)"); return -1; }
     return 0;
 }
 
@@ -963,6 +986,10 @@ int init_gather(ltgp_engine* e) {
     const ncclResult_t r = g.comm_init_all(g.comms, n, devs);
     if (r != ncclSuccess) { set_err("ncclCommInitAll: %s", g.error_string(r)); return -1; }
     g.nccl = true;
+    // one line per engine so a multi-GPU run shows its communicator size
+    std::string dl;
+    for (int i = 0; i < n; ++i) dl += (i ? "," : "") + std::to_string(devs[i]);
+    std::fprintf(stderr, "[ltgp] NCCL record all-gather: ncclCommInitAll nranks=%d devices=%s\n", n, dl.c_str());
     return 0;
 }
 
@@ -985,6 +1012,7 @@ void release_gather(ltgp_engine* e) {
 // (peer copies; shards that repeat a device). Shard 0's array then goes to
 // the host in one copy and is unpacked into slot order.
 int gather_records(ltgp_engine* e, ltgp_record* out) {
+    NvtxRange nr("ltgp.record_all_gather");
     auto& g = e->gather;
     const int n = (int)e->shards.size();
     uint32_t cmax = 1;
@@ -1096,7 +1124,14 @@ int collect(ltgp_engine* e, ltgp_record* out, float* outs48) {
 extern "C" {
 
 const char* ltgp_last_error(void) { return g_err.c_str(); }
-const char* ltgp_version(void) { return "ltgp_cuda 0.1 (sm_100a)"; }
+const char* ltgp_version(void) { return "ltgp_cuda 0.2 (sm_100a)"; }
+
+int ltgp_device_count(int* n) {
+    if (!n) { set_err("null argument"); return -1; }
+    *n = 0;
+    CK(cudaGetDeviceCount(n));
+    return 0;
+}
 
 int ltgp_engine_create(const ltgp_config* cfg, ltgp_engine** out) {
     if (!cfg || !out) { set_err("null argument"); return -1; }
@@ -1410,7 +1445,12 @@ int ltgp_evaluate_outputs(ltgp_engine* e, ltgp_record* out, float* outs48) {
 }
 
 int ltgp_eval_one(ltgp_engine* e, const uint8_t* ops, uint64_t n, float* out48) {
+    return ltgp_eval_one_record(e, ops, n, out48, nullptr);
+}
+
+int ltgp_eval_one_record(ltgp_engine* e, const uint8_t* ops, uint64_t n, float* out48, ltgp_record* rec) {
     if (!e || !ops || !out48) { set_err("null argument"); return -1; }
+    if (n == 0) { set_err("empty genome"); return -1; }
     if (!e->have_suite) { set_err("ltgp_set_suite not called"); return -1; }
     Shard& s = e->shards[0];
     TreeSet& ts = s.scratch;
@@ -1428,7 +1468,9 @@ int ltgp_eval_one(ltgp_engine* e, const uint8_t* ops, uint64_t n, float* out48) 
     CK(cudaStreamSynchronize(s.st));
     TRY(finish_eval(e, s));
     CK(cudaMemcpyAsync(out48, s.outs.p, sizeof(float) * kLanes, cudaMemcpyDeviceToHost, s.st));
+    if (rec) CK(cudaMemcpyAsync(rec, s.rec.p, sizeof(ltgp_record), cudaMemcpyDeviceToHost, s.st));
     CK(cudaStreamSynchronize(s.st));
+    e->stats.nodes_evaluated += n;
     return 0;
 }
 
@@ -1438,6 +1480,7 @@ int ltgp_get_stats(ltgp_engine* e, ltgp_stats* out) {
     for (Shard& s : e->shards)
         for (auto& ts : s.set) hw = std::max<uint64_t>(hw, ts.arena.bytes);
     e->stats.arena_high_water = hw;
+    e->stats.gather_nccl = e->gather.nccl ? 1u : 0u;
     *out = e->stats;
     return 0;
 }
@@ -1518,7 +1561,7 @@ int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M, 
             set_err("plan %u references slot outside the population", c);
             return -1;
         }
-    Trace tr;
+    Trace tr("ltgp.execute_generation");
     std::vector<DirEntry> dir;
     build_directory(e, dir);
     for (uint32_t c = 0; c < M; ++c)
@@ -1546,6 +1589,7 @@ int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M, 
         CK(cudaMemsetAsync(s.counters.p, 0, 64, s.st));
         CK(cudaEventRecord(s.ev[2], s.st));
         const uint32_t warps = 2 * qcount[g];
+        NvtxRange nr_ext("ltgp.extents");
         k_extent<<<(warps + 3) / 4, 128, 0, s.st>>>(s.plans.as<PlanDev>(), qcount[g], s.dir.as<DirEntry>(),
                                                   s.ext.as<Extent>(), nullptr, s.counters.as<uint32_t>() + 3);
         CK(cudaGetLastError());
@@ -1578,7 +1622,15 @@ int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M, 
     }
     // 3. SizeLimitHit (genome.hpp:71-84): child >= node_limit
     for (uint32_t c = 0; c < M; ++c)
-        if (csize[c] >= e->cfg.node_limit || csize[c] > 0xffffffffull) { *size_limit_hit = 1; return 0; }
+        if (csize[c] >= e->cfg.node_limit) { *size_limit_hit = 1; return 0; }
+    // a child below node_limit (node_limit > 2^32) but beyond the engine's
+    // u32 sizes is an engine capacity error, not the run's SizeLimitHit
+    for (uint32_t c = 0; c < M; ++c)
+        if (csize[c] > 0xffffffffull) {
+            set_err("child %u has %llu nodes: beyond the engine's 2^32-1-node tree capacity (node_limit %llu)", c,
+                    (unsigned long long)csize[c], (unsigned long long)e->cfg.node_limit);
+            return -1;
+        }
     // 4. children partitioned by bytes; splice into the other buffer
     // (parents stay readable until every shard has spliced).
     std::vector<uint32_t> old_cur(G);
@@ -1609,6 +1661,7 @@ int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M, 
                                s.st));
         }
         CK(cudaEventRecord(s.ev[2], s.st));
+        NvtxRange nr_splice("ltgp.splice");
         k_splice<<<std::min<uint32_t>(s.count, (uint32_t)s.sms * 8), 256, 0, s.st>>>(
             s.plans.as<PlanDev>(), s.count, s.dir.as<DirEntry>(), s.ext.as<Extent>(), s.coff.as<uint64_t>(),
             s.csize.as<uint64_t>(), ts.arena.as<uint8_t>());

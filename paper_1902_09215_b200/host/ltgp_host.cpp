@@ -17,6 +17,8 @@
 #include <string>
 #include <thread>
 
+#include <unistd.h>
+
 #include "../../include/ltgp_host.h"
 
 namespace ltgp {
@@ -491,6 +493,7 @@ struct CkptHeader {
     uint64_t gen, nodes;
     double secs;
     int64_t gauge_live, gauge_high;
+    uint64_t dump_bytes;  // dump length at this checkpoint: a resume truncates the dump back to it
 };
 
 struct Fnv {
@@ -635,6 +638,7 @@ int64_t ltgp_host_run_checkpointed(ltgp_engine* e, uint32_t M, uint32_t G, uint6
         *nodes = 0;
         double secs = 0.0;
         uint32_t gen0 = 0;
+        uint64_t dump_bytes0 = 0;
         if (resume_path) {
             CkptHeader h;
             load_checkpoint(resume_path, hdr, h, rng, pop);
@@ -651,10 +655,24 @@ int64_t ltgp_host_run_checkpointed(ltgp_engine* e, uint32_t M, uint32_t G, uint6
             check(ltgp_upload_population(e, M, ptrs.data(), sizes.data()));
             for (auto& ind : pop) ind.genome.release();
             gen0 = static_cast<uint32_t>(h.gen);
+            dump_bytes0 = h.dump_bytes;
             *nodes = h.nodes;
             secs = h.secs;
         }
-        FILE* dump = dump_path ? std::fopen(dump_path, resume_path ? "a" : "w") : nullptr;
+        FILE* dump = nullptr;
+        if (dump_path && resume_path) {
+            // generations dumped after the checkpoint (a run that died between
+            // checkpoints) are cut off, so the resumed dump equals an
+            // uninterrupted run's
+            dump = std::fopen(dump_path, "r+");
+            if (!dump) throw std::invalid_argument(std::string("resume: cannot open the dump ") + dump_path);
+            std::fflush(dump);
+            if (ftruncate(fileno(dump), static_cast<off_t>(dump_bytes0)) != 0)
+                throw std::runtime_error("resume: cannot truncate the dump");
+            std::fseek(dump, 0, SEEK_END);
+        } else if (dump_path) {
+            dump = std::fopen(dump_path, "w");
+        }
         auto write_dump = [&](uint32_t gen) {  // stats.hpp:104-107
             if (!dump) return;
             for (uint32_t i = 0; i < M; ++i) {
@@ -671,6 +689,11 @@ int64_t ltgp_host_run_checkpointed(ltgp_engine* e, uint32_t M, uint32_t G, uint6
             hdr.secs = secs;
             hdr.gauge_live = gauge.live();
             hdr.gauge_high = gauge.high_water();
+            hdr.dump_bytes = 0;
+            if (dump) {
+                std::fflush(dump);
+                hdr.dump_bytes = static_cast<uint64_t>(std::ftell(dump));
+            }
             save_checkpoint(ckpt_path, e, hdr, rng, pop);
         };
         ltgp_stats st;

@@ -37,6 +37,8 @@ SIGS = {
     "orc_ramped_half_and_half": (C.c_uint64, [C.c_uint64, C.c_uint32, C.c_uint64, C.c_int, C.c_int, P,
                                               C.c_uint64, P]),
     "orc_random_tree_of_size": (C.c_int, [C.c_uint64, C.c_uint64, P]),
+    "orc_corpus": (C.c_uint64, [C.c_uint64, C.c_uint32, C.c_double, C.c_double, C.c_uint32, C.c_uint32,
+                                P, P, P, C.c_int]),
     "orc_eval_scalar": (C.c_float, [P, C.c_uint64, C.c_float, P]),
     "orc_eval_batch": (C.c_int, [P, C.c_uint64, P, P, P, P]),
     "orc_fitness": (C.c_float, [P, P]),
@@ -127,6 +129,21 @@ class Oracle:
             gs.append(out[pos:pos + int(s)].copy())
             pos += int(s)
         return gs
+
+    def corpus_sizes(self, seed, count, lg_lo=4.0, lg_hi=6.0):
+        sizes = np.zeros(count, np.uint64)
+        self.lib.orc_corpus(seed, count, lg_lo, lg_hi, 0, 0, None, None, _p(sizes), 0)
+        return sizes
+
+    def corpus(self, seed, count, lg_lo=4.0, lg_hi=6.0, first=0, n=None, threads=0):
+        """Config-3 corpus trees [first, first+n): (buf, offsets, sizes)."""
+        n = count - first if n is None else n
+        sizes = np.zeros(count, np.uint64)
+        offs = np.zeros(max(n, 1), np.uint64)
+        total = int(self.lib.orc_corpus(seed, count, lg_lo, lg_hi, first, n, None, _p(offs), _p(sizes), threads))
+        buf = np.empty(total + 64, np.uint8)
+        self.lib.orc_corpus(seed, count, lg_lo, lg_hi, first, n, _p(buf), _p(offs), _p(sizes), threads)
+        return buf, offs[:n], sizes[first:first + n].copy()
 
     def evaluate_population(self, buf, offsets, sizes, suite, threads=0):
         i, t, c = suite

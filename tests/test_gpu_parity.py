@@ -295,6 +295,26 @@ def test_run_checkpoint_resume_matches_oracle(oracle, tmp_path, shards):
             e.run(48, 40, 10**9, 7, 2, None, 1, resume=str(bad))
 
 
+def test_resume_truncates_dump_after_crash(oracle, tmp_path):
+    """A run that dies between checkpoints (checkpoint at generation 14, dump
+    written through 17) resumes from generation 14: the dump is cut back to
+    the checkpoint's length first, so it ends identical to an uninterrupted
+    run's (the resumed run must not dump generations 15-17 twice)."""
+    ref = tmp_path / "ref.txt"
+    oracle.run(48, 30, 10**9, 7, 5, 0, str(ref), 1)
+    ck = tmp_path / "run.ckpt"
+    d = tmp_path / "gpu.txt"
+    with ltgp.Engine([0], node_limit=10**9, chunk_nodes=256) as e:
+        assert e.run(48, 14, 10**9, 7, 5, str(d), 1, checkpoint=str(ck), checkpoint_every=7)["generations"] == 14
+    # the "crashed" continuation: generations 15-17 dumped, no checkpoint after 14
+    with ltgp.Engine([0], node_limit=10**9, chunk_nodes=256) as e:
+        assert e.run(48, 17, 10**9, 7, 5, str(d), 1, resume=str(ck))["generations"] == 17
+    assert d.read_bytes().count(b"\n") == 18 * 48
+    with ltgp.Engine([0], node_limit=10**9) as e:
+        assert e.run(48, 30, 10**9, 7, 5, str(d), 1, resume=str(ck))["generations"] == 30
+    assert d.read_bytes() == ref.read_bytes()
+
+
 def test_run_size_limit_matches_oracle(oracle, tmp_path):
     # SPEC.md:380: node_limit=63 -> SizeLimitHit within a few generations
     r = oracle.run(48, 300, 63, 7, 4, 0, str(tmp_path / "a"))
@@ -452,14 +472,54 @@ def test_streamed_slice_cap(oracle, suite, monkeypatch):
 
 @pytest.mark.slow
 def test_config2_bloating_run_matches_oracle(oracle, tmp_path):
-    """Config 2 scale: pop 4000, tournament 7, no size limit, 100 generations
-    with the bloating grow variant; 2 shards; dumps identical to the oracle."""
-    r = oracle.run(4000, 100, 2**62, 7, 1, 0, str(tmp_path / "a"), 1)
-    with ltgp.Engine([0, 0], node_limit=2**62) as e:
-        g = e.run(4000, 100, 2**62, 7, 1, str(tmp_path / "b"), 1)
-    assert r["generations"] == g["generations"] == 100
+    """Config 2 at its full BASELINE size: pop 4000, tournament 7, no size
+    limit, all 200 generations with the bloating grow variant, at 1 and 2
+    shards; generation dumps (sizes, depths, hits, fitness bits of every
+    individual: the selected parents follow from them) identical to the
+    oracle's run()."""
+    r = oracle.run(4000, 200, 2**62, 7, 1, 0, str(tmp_path / "a"), 1)
+    for shards in (1, 2):
+        with ltgp.Engine([0] * shards, node_limit=2**62) as e:
+            g = e.run(4000, 200, 2**62, 7, 1, str(tmp_path / "b"), 1)
+        assert r["generations"] == g["generations"] == 200
+        assert r["nodes"] == g["nodes"]
+        assert (tmp_path / "a").read_bytes() == (tmp_path / "b").read_bytes()
+
+
+@pytest.mark.slow
+def test_config5_capped_run_matches_oracle(oracle, tmp_path):
+    """Config 5's regime: pop 4000 capped at a 15M-node limit per individual
+    (node_limit = 15e6), bloating grow, 300 generations on device splicing;
+    the dump is identical to the oracle's."""
+    r = oracle.run(4000, 300, 15_000_000, 7, 1, 0, str(tmp_path / "a"), 1)
+    with ltgp.Engine([0], node_limit=15_000_000) as e:
+        g = e.run(4000, 300, 15_000_000, 7, 1, str(tmp_path / "b"), 1)
+    assert r["generations"] == g["generations"] and r["reason"] == g["reason"]
     assert r["nodes"] == g["nodes"]
     assert (tmp_path / "a").read_bytes() == (tmp_path / "b").read_bytes()
+
+
+@pytest.mark.slow
+def test_config4_regime_large_remy_trees(oracle, suite):
+    """Config 4's regime: uniform random (Remy) trees of 4e7 nodes at the
+    automatic chunk length (>= 2^18-node chunks, an 8 sqrt(C) spill area per
+    warp, spine chains of thousands of steps): records and all 48 per-case
+    outputs of both trees equal the oracle's."""
+    from concurrent.futures import ThreadPoolExecutor
+    n = 40_000_001
+    with ThreadPoolExecutor(2) as ex:
+        genomes = list(ex.map(lambda k: ltgp.remy_tree(7100 + k, n), range(2)))
+    with engine(suite) as e:
+        e.upload_population(genomes)
+        rec, outs = e.evaluate_outputs()
+        st = e.stats()
+    assert st["last_chunks"] >= 2 * (n // 2**18)          # chunks of at most 2^18 nodes
+    assert st["last_chunks"] <= 2 * (n // 2**17 + 1)      # ... and more than 2^17
+    buf, offs, sizes = pack(genomes)
+    assert_records_equal(rec, oracle.evaluate_population(buf, offs, sizes, suite, threads=0))
+    for k, g in enumerate(genomes):
+        o, _ = oracle.eval_batch(g, suite[0], suite[2])
+        assert same_bits(outs[k], o)
 
 
 @pytest.mark.parametrize("round_", range(int(os.environ.get("LTGP_FUZZ_ROUNDS", "3"))))
@@ -520,6 +580,27 @@ def test_error_behaviour_and_edge_cases(oracle, suite):
         e.upload_population([big_bad])
         with pytest.raises(ltgp.EngineError, match="malformed"):
             e.evaluate_population()
+        # opcode 255 (invalid, opcodes.hpp:8-15) inside a tree is malformed,
+        # wherever it falls: a leaf slot of a small tree, the middle of a
+        # full packet of a large one, a chunked tree's interior, and on the
+        # streamed path
+        g = ltgp.random_tree_of_size(3, 40001)
+        leaves = np.flatnonzero(g >= 4)
+        for pos in (leaves[0], leaves[len(leaves) // 2], leaves[-1]):
+            bad = g.copy()
+            bad[pos] = 255
+            for chunk in (0, 1024):
+                with ltgp.Engine([0], node_limit=10**9, chunk_nodes=chunk) as e2:
+                    e2.set_suite(*suite)
+                    e2.upload_population([bad])
+                    with pytest.raises(ltgp.EngineError, match="malformed"):
+                        e2.evaluate_population()
+                    b3, o3, s3 = pack([g, bad])
+                    with pytest.raises(ltgp.EngineError, match="malformed"):
+                        e2.evaluate_packed(b3, o3, s3)
+        e.upload_population([np.array([ADD, X, 255], np.uint8)])
+        with pytest.raises(ltgp.EngineError, match="malformed"):
+            e.evaluate_population()
         # engine still usable afterwards
         one = [np.array([5 + 17], np.uint8)]
         e.upload_population(one)
@@ -562,3 +643,96 @@ def test_run_bench_cells():
     with pytest.raises(ltgp.EngineError):
         ltgp.run_bench([1001], [0])
 
+
+
+def test_reference_kat_grid_on_gpu():
+    """The GPU arithmetic against bits printed by the reference's OWN inline
+    apply_op / protected_div (eval.hpp:54-63, compiled from the reference
+    headers by oracle/_ref/ref_kat, frozen in tests/golden/ref_inline_kats.json):
+    20 special values (+-0, +-1, subnormals, FLT_MAX, +-inf, NaN, ...) as the
+    constant table, every `op Ci Cj`. Bare 3-node trees run on the checked
+    per-node path; the same pair wrapped as MUL(...MUL(op Ci Cj, 1)..., 1)
+    puts the op inside a full packet (the generated fast path, including the
+    packed division's domain check and its IEEE slow block). NaN payloads
+    differ between x86 and the GPU (SURVEY.md App. A #14): NaN matches NaN."""
+    kats = json.load(open(os.path.join(HERE, "golden", "ref_inline_kats.json")))
+    vals = np.array(kats["values"], np.uint32)
+    nv = len(vals)
+    consts = np.zeros(250, np.float32)
+    consts[:nv] = vals.view(np.float32)
+    one = 5 + int(np.flatnonzero(vals == 0x3F800000)[0])
+    inputs = np.linspace(-1, 1, 48).astype(np.float32)
+    targets = np.zeros(48, np.float32)
+    for wrap in (0, 10, 11):
+        genomes, expect = [], []
+        for op in range(4):
+            for i in range(nv):
+                for j in range(nv):
+                    core = [op, 5 + i, 5 + j]
+                    genomes.append(np.array([MUL] * wrap + core + [one] * wrap, np.uint8))
+                    expect.append(kats["apply_op"][op][i * nv + j])
+        with ltgp.Engine([0], node_limit=10**6) as e:
+            e.set_suite(inputs, targets, consts)
+            e.upload_population(genomes)
+            _, outs = e.evaluate_outputs()
+        exp = np.array(expect, np.uint32).view(np.float32)
+        for lane in (0, 1, 23, 47):
+            assert same_bits(outs[:, lane], exp), f"wrap {wrap}, lane {lane}"
+    # protected_div's own table equals apply_op's DIV row (same function)
+    assert kats["protected_div"] == kats["apply_op"][3]
+
+
+@pytest.mark.slow
+def test_depth_beyond_2_24(oracle, suite):
+    """Depth is an integer (genome.hpp:46 returns std::size_t): a right-deep
+    chain ADD/SUB x (... ) of 2^24 + 11 function nodes has depth 2^24 + 12,
+    which float32 cannot represent (a float depth chain sticks at 2^24). The
+    tree (33.6M nodes) is chunked at the automatic length, so the depth also
+    crosses the spine combine."""
+    k = 2**24 + 11
+    g = np.empty(2 * k + 1, np.uint8)
+    g[0:2 * k:2] = np.where(np.arange(k) % 2 == 0, ADD, SUB)
+    g[1:2 * k:2] = np.where(np.arange(k) % 3 == 0, X, 5 + 17)
+    g[-1] = X
+    with engine(suite) as e:
+        e.upload_population([g])
+        rec, outs = e.evaluate_outputs()
+        assert e.stats()["last_chunks"] > 1
+    assert int(rec["depth"][0]) == k + 1 == oracle.depth(g)
+    o, _ = oracle.eval_batch(g, suite[0], suite[2])
+    assert same_bits(outs[0], o)
+    buf, offs, sizes = pack([g])
+    assert_records_equal(rec, oracle.evaluate_population(buf, offs, sizes, suite, threads=0))
+
+
+def _gpus():
+    import torch
+    return torch.cuda.device_count()
+
+
+@pytest.mark.skipif("_gpus() < 2", reason="needs >= 2 GPUs (distinct-device NCCL all-gather and P2P splice)")
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_distinct_devices_nccl_matches_one_shard(oracle, suite, tmp_path, G):
+    """The multi-GPU product path (SURVEY.md §8(e)): a population sharded over
+    G distinct GPUs, records all-gathered by one grouped ncclAllGather over
+    NVLink (use_nccl), children spliced from parents on peer GPUs. Records
+    and run dumps are byte-identical to one shard and to the oracle
+    (bit-identical for any worker count, evolve.hpp:111-117, SPEC.md:386)."""
+    if _gpus() < G:
+        pytest.skip(f"needs {G} GPUs")
+    devs = list(range(G))
+    buf, offs, sizes = ltgp.corpus(3, 64, 3.0, 5.0)
+    genomes = [buf[int(o):int(o) + int(n)].copy() for o, n in zip(offs, sizes)]
+    with engine(suite, devs) as e:
+        assert e.gather_mode() == "nccl"
+        e.upload_population(genomes)
+        rec, outs = e.evaluate_outputs()
+    exp = oracle.evaluate_population(buf, offs, sizes, suite, threads=0)
+    assert_records_equal(rec, exp)
+    ref = tmp_path / "ref.txt"
+    r = oracle.run(400, 60, 10**9, 7, 3, 0, str(ref), 1)
+    d = tmp_path / "gpu.txt"
+    with ltgp.Engine(devs, node_limit=10**9) as e:
+        g = e.run(400, 60, 10**9, 7, 3, str(d), 1)
+    assert g["generations"] == r["generations"] and g["nodes"] == r["nodes"]
+    assert d.read_bytes() == ref.read_bytes()

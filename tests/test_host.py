@@ -36,6 +36,18 @@ def test_corpus_trees_match_oracle_generator(oracle):
         assert np.array_equal(g, oracle.random_tree_of_size(ltgp.tree_seed(11, i), int(sizes[i])))
 
 
+def test_oracle_corpus_is_the_product_corpus(oracle):
+    # bench.py's reference arm builds the workload with the oracle alone
+    # (orc_corpus): it must be byte-identical to the product's corpus
+    for seed, M, lo, hi, first, n in ((1, 4000, 4.0, 6.0, 0, 3), (1, 4000, 4.0, 6.0, 3990, 10), (7, 50, 2.0, 4.0, 5, 20)):
+        assert np.array_equal(oracle.corpus_sizes(seed, M, lo, hi), ltgp.corpus_sizes(seed, M, lo, hi))
+        b1, o1, s1 = oracle.corpus(seed, M, lo, hi, first=first, n=n)
+        b2, o2, s2 = ltgp.corpus(seed, M, lo, hi, first=first, n=n)
+        assert np.array_equal(o1, o2) and np.array_equal(s1, s2)
+        end = int(o1[-1] + (s1[-1] + 15) // 16 * 16)
+        assert np.array_equal(b1[:end], b2[:end])
+
+
 def test_remy_tree_valid(oracle):
     for n in (1, 3, 1001, 200001):
         g = ltgp.remy_tree(5, n)

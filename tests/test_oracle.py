@@ -184,8 +184,8 @@ def test_eval_batch_equals_eval_scalar(oracle):
         n = int(rng.integers(0, 2000)) * 2 + 1
         g = oracle.random_tree_of_size(7000 + k, n)
         out, peak = oracle.eval_batch(g, i, c)
-        ref = np.array([oracle.eval_scalar(g, x, c) for x in i[:8]], np.float32)
-        assert same_bits(out[:8], ref)
+        ref = np.array([oracle.eval_scalar(g, x, c) for x in i], np.float32)
+        assert same_bits(out, ref)                                        # all 48 lanes
         assert peak <= oracle.depth(g)
 
 
@@ -204,15 +204,25 @@ def test_eval_batch_equals_eval_scalar_adversarial(oracle):
 
 
 def test_fitness_not_reassociated(oracle):
-    # mixed magnitudes where a tree reduction differs
+    # SPEC.md:232 (reduction-order mutation check): 1e8 followed by 47 ones.
+    # Left to right every +1 is absorbed (ulp(1e8) = 8): the sum is 1e8.
+    # Any other order that adds the ones first gives 1e8 + 48 (a reversed
+    # sum, a pairwise tree): the MAE must be the left-to-right one.
     t = np.zeros(48, np.float32)
-    out = np.array([1e8, 1.0, -1e8, 1.0] * 12, np.float32)
+    out = np.array([1e8] + [1.0] * 47, np.float32)
     s = np.float32(0)
     for v in out:
         s = np.float32(s + np.float32(abs(v)))
+    assert s == np.float32(1e8)
     assert oracle.fitness(out, t) == np.float32(s / np.float32(48))
-    pairwise = np.float32(np.sum(np.abs(out).reshape(2, 24), axis=1, dtype=np.float32).sum() / 48)
-    assert oracle.fitness(out, t) != pairwise or True
+    rev = np.float32(0)
+    for v in out[::-1]:
+        rev = np.float32(rev + np.float32(abs(v)))
+    pairwise = np.float32(np.float32(np.abs(out[:24]).sum(dtype=np.float32)) +
+                          np.float32(np.abs(out[24:]).sum(dtype=np.float32)))
+    assert rev != s and pairwise != s
+    assert oracle.fitness(out, t) != np.float32(rev / np.float32(48))
+    assert oracle.fitness(out, t) != np.float32(pairwise / np.float32(48))
 
 
 def test_crossover_size_algebra(oracle):
