@@ -71,6 +71,9 @@ typedef struct {
     uint32_t kernel_launches;   /* engine kernels launched by the last call */
     uint32_t gather_nccl;       /* 1: records are all-gathered by NCCL (distinct devices, use_nccl) */
     double keval_seconds;       /* k_eval alone, max over shards (resident evaluations; 0 when streamed) */
+    uint64_t live_genomes_high_water; /* streaming memory mode: most live genomes (parents not yet
+                                         retired + children built) seen at a wave boundary */
+    uint64_t arena_used_high_water;   /* streaming memory mode: most arena bytes holding live genomes */
 } ltgp_stats;
 
 /* Generation statistics of the current population (GenerationStats,
@@ -154,6 +157,15 @@ int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M,
 /* Generation statistics of the current population (after an evaluation or
    execute_generation): no host pass over the records. */
 int ltgp_generation_stats(ltgp_engine* e, ltgp_gen_stats* out);
+
+/* RunConfig::streaming_memory (evolve.hpp:45; execute_generation's "in
+   streaming mode parents are retired as their last planned use completes",
+   evolve.hpp:111-114): on = 1 splices each generation's children, in plan
+   order and waves of `wave` children (0 = keep the current, default 256), into
+   the parents' own arena by first fit, releasing a parent's bytes after the
+   wave of its last planned use. Results are identical to the default
+   double-buffered mode (2M); single-shard engines only. */
+int ltgp_set_streaming(ltgp_engine* e, int on, uint32_t wave);
 
 /* RunConfig::memory_budget_bytes (evolve.hpp:44): genome bytes a generation
    may plan (parents + children); 0 (the default) disables the check. */

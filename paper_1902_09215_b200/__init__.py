@@ -56,7 +56,8 @@ class _Stats(C.Structure):
                 ("arena_high_water", C.c_uint64), ("last_chunks", C.c_uint64),
                 ("last_fallback_items", C.c_uint64), ("last_exits", C.c_uint64),
                 ("last_window_adjusts", C.c_uint64), ("last_spine_steps", C.c_uint64),
-                ("kernel_launches", C.c_uint32), ("gather_nccl", C.c_uint32), ("keval_seconds", C.c_double)]
+                ("kernel_launches", C.c_uint32), ("gather_nccl", C.c_uint32), ("keval_seconds", C.c_double),
+                ("live_genomes_high_water", C.c_uint64), ("arena_used_high_water", C.c_uint64)]
 
 
 _cuda = None
@@ -72,6 +73,7 @@ _CUDA_SIGS = {
     "ltgp_engine_destroy": (C.c_int, [_P]),
     "ltgp_set_suite": (C.c_int, [_P, _P, _P, _P]),
     "ltgp_set_memory_budget": (C.c_int, [_P, C.c_uint64]),
+    "ltgp_set_streaming": (C.c_int, [_P, C.c_int, C.c_uint32]),
     "ltgp_generation_stats": (C.c_int, [_P, _P]),
     "ltgp_upload_population": (C.c_int, [_P, C.c_uint32, _P, _P]),
     "ltgp_upload_packed": (C.c_int, [_P, C.c_uint32, _P, C.c_uint64, _P, _P]),
@@ -309,6 +311,16 @@ class Engine:
         c = np.ascontiguousarray(constants, np.float32)
         assert i.size == LANES and t.size == LANES and c.size == CONSTANTS
         _check(self._lib.ltgp_set_suite(self._h, _ptr(i), _ptr(t), _ptr(c)))
+
+    def set_streaming(self, on: bool = True, wave: int = 0):
+        """RunConfig::streaming_memory (evolve.hpp:45): children spliced in
+        waves into the parents' arena, parents released after their last
+        planned use (ltgp_set_streaming)."""
+        _check(self._lib.ltgp_set_streaming(self._h, 1 if on else 0, wave))
+
+    def set_memory_budget(self, nbytes: int):
+        """RunConfig::memory_budget_bytes (evolve.hpp:44)."""
+        _check(self._lib.ltgp_set_memory_budget(self._h, nbytes))
 
     def upload_population(self, genomes: Sequence[np.ndarray]):
         gs = [np.ascontiguousarray(g, np.uint8) for g in genomes]

@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -284,6 +285,14 @@ struct ltgp_engine {
     bool have_suite = false;
     uint32_t M = 0;
     uint64_t memory_budget = 0;  // planned generation bytes allowed (0: no check)
+    // RunConfig::streaming_memory (evolve.hpp:45, :111-114): children are
+    // spliced in waves of stream_wave into the parents' own arena, and a
+    // parent's bytes are released for reuse after the wave holding its last
+    // planned use (a first-fit heap over the arena)
+    bool streaming = false;
+    uint32_t stream_wave = 256;
+    uint64_t live_high_water = 0;    // live genomes (parents not yet retired + children built)
+    uint64_t used_high_water = 0;    // arena bytes holding live genomes
     ltgp_stats stats;
     HostBuf staging;
     // record all-gather of a multi-shard population: every
@@ -1266,6 +1275,14 @@ int ltgp_generation_stats(ltgp_engine* e, ltgp_gen_stats* out) {
     return 0;
 }
 
+int ltgp_set_streaming(ltgp_engine* e, int on, uint32_t wave) {
+    if (!e) { set_err("null engine"); return -1; }
+    if (on && e->shards.size() != 1) { set_err("streaming memory mode needs a single-shard engine"); return -1; }
+    e->streaming = on != 0;
+    if (wave) e->stream_wave = wave;
+    return 0;
+}
+
 int ltgp_set_memory_budget(ltgp_engine* e, uint64_t bytes) {
     if (!e) { set_err("null engine"); return -1; }
     e->memory_budget = bytes;
@@ -1481,6 +1498,8 @@ int ltgp_get_stats(ltgp_engine* e, ltgp_stats* out) {
         for (auto& ts : s.set) hw = std::max<uint64_t>(hw, ts.arena.bytes);
     e->stats.arena_high_water = hw;
     e->stats.gather_nccl = e->gather.nccl ? 1u : 0u;
+    e->stats.live_genomes_high_water = e->live_high_water;
+    e->stats.arena_used_high_water = e->used_high_water;
     *out = e->stats;
     return 0;
 }
@@ -1521,6 +1540,8 @@ int ltgp_download_genome(ltgp_engine* e, uint32_t idx, uint8_t* buf, uint64_t ca
 // ---------------------------------------------------------------------------
 // Crossover on device: execute_generation (evolve.hpp:111-117).
 // ---------------------------------------------------------------------------
+
+
 namespace {
 
 // Directory of the current population: per global slot, its device address
@@ -1549,6 +1570,145 @@ int upload_directory(ltgp_engine* e, Shard& s, const std::vector<DirEntry>& dir)
 }  // namespace
 
 extern "C" {
+
+// Streaming memory mode (RunConfig::streaming_memory, evolve.hpp:45,
+// :111-114): the paper's "specialised
+// heap for the population". Children are placed, in plan order and in waves
+// of stream_wave, into the parents' own arena by first fit over its free
+// intervals; after the wave that holds a parent's last planned use, the
+// parent's bytes join the free list (released in the sequential coordinator,
+// as SPEC.md:392 asks: here the host computes the whole placement before
+// any kernel runs, since every child size is known from the crossover
+// algebra). Waves splice in stream order, so a wave never overwrites a
+// parent an earlier or the same wave still reads. Live genomes (parents not
+// yet retired + children built) and arena bytes in use are tracked at every
+// wave: live_high_water / used_high_water.
+static int splice_streaming(ltgp_engine* e, const ltgp_plan* plans, uint32_t M, const std::vector<uint64_t>& csize) {
+    Shard& s = e->shards[0];
+    TreeSet& ts = s.set[s.cur];
+    const uint32_t P = ts.count;  // parents
+    const uint32_t W = std::max<uint32_t>(1, e->stream_wave);
+    std::vector<int64_t> last(P, -1);
+    for (uint32_t c = 0; c < M; ++c) {
+        last[plans[c].mum_index] = c;
+        last[plans[c].dad_index] = c;
+    }
+    // free intervals [start, end), address ordered; the tail is unbounded
+    std::map<uint64_t, uint64_t> fr;
+    {
+        std::vector<std::pair<uint64_t, uint64_t>> occ(P);
+        for (uint32_t i = 0; i < P; ++i) occ[i] = {ts.h_off[i], ts.h_off[i] + ceil16(ts.h_size[i])};
+        std::sort(occ.begin(), occ.end());
+        uint64_t at = 0;
+        for (const auto& o : occ) {
+            if (o.first > at) fr[at] = o.first;
+            at = std::max(at, o.second);
+        }
+        fr[at] = ~0ull;
+    }
+    auto release = [&](uint64_t a, uint64_t b) {
+        auto it = fr.lower_bound(a);
+        if (it != fr.end() && it->first == b) {  // merge with the next interval
+            b = it->second;
+            it = fr.erase(it);
+        }
+        if (it != fr.begin()) {
+            auto pv = std::prev(it);
+            if (pv->second == a) {  // merge with the previous interval
+                pv->second = b;
+                return;
+            }
+        }
+        fr[a] = b;
+    };
+    std::vector<std::vector<uint32_t>> retire((M + W - 1) / W + 1);
+    for (uint32_t p = 0; p < P; ++p) retire[last[p] < 0 ? 0 : (uint32_t)(last[p] / W) + 1].push_back(p);
+    uint64_t live_bytes = 0;
+    for (uint32_t i = 0; i < P; ++i) live_bytes += ceil16(ts.h_size[i]);
+    int64_t live = P;
+    uint64_t used_hw = live_bytes, end = 0;
+    int64_t live_hw = live;
+    for (uint32_t p : retire[0]) {  // parents no plan uses
+        release(ts.h_off[p], ts.h_off[p] + ceil16(ts.h_size[p]));
+        live_bytes -= ceil16(ts.h_size[p]);
+        --live;
+    }
+    for (uint32_t i = 0; i < P; ++i) end = std::max<uint64_t>(end, ts.h_off[i] + ceil16(ts.h_size[i]));
+    std::vector<uint64_t> coff(M);
+    for (uint32_t w0 = 0, wi = 1; w0 < M; w0 += W, ++wi) {
+        const uint32_t w1 = std::min(M, w0 + W);
+        for (uint32_t c = w0; c < w1; ++c) {
+            const uint64_t need = ceil16(csize[c]);
+            auto it = fr.begin();
+            while (it->second - it->first < need) ++it;  // the tail interval always fits
+            coff[c] = it->first;
+            const uint64_t a = it->first + need, b = it->second;
+            fr.erase(it);
+            if (a < b) fr[a] = b;
+            end = std::max(end, coff[c] + need);
+            live_bytes += need;
+            ++live;
+        }
+        live_hw = std::max(live_hw, live);
+        used_hw = std::max(used_hw, live_bytes);
+        for (uint32_t p : retire[wi]) {  // last planned use was in this wave
+            release(ts.h_off[p], ts.h_off[p] + ceil16(ts.h_size[p]));
+            live_bytes -= ceil16(ts.h_size[p]);
+            --live;
+        }
+    }
+    e->live_high_water = std::max<uint64_t>(e->live_high_water, (uint64_t)live_hw);
+    e->used_high_water = std::max<uint64_t>(e->used_high_water, used_hw);
+    CK(cudaSetDevice(s.dev));
+    // the arena must hold the placement; growing keeps the parents' bytes
+    const uint64_t need_bytes = end + 64;
+    if (need_bytes > ts.arena.bytes) {
+        DevBuf grown;
+        TRY(grown.ensure(need_bytes, s.dev));
+        CK(cudaMemcpyAsync(grown.p, ts.arena.p, ts.arena.bytes, cudaMemcpyDeviceToDevice, s.st));
+        CK(cudaStreamSynchronize(s.st));
+        ts.arena.release();
+        ts.arena = grown;
+        grown.p = nullptr;  // owned by ts.arena now
+        std::vector<DirEntry> dir;  // the parents moved: rebuild the directory
+        build_directory(e, dir);
+        TRY(upload_directory(e, s, dir));
+    }
+    TRY(s.coff.ensure(sizeof(uint64_t) * M, s.dev));
+    TRY(s.h_coff.ensure(sizeof(uint64_t) * M * 2));
+    uint8_t* hb = s.h_coff.as<uint8_t>();
+    std::memcpy(hb, coff.data(), sizeof(uint64_t) * M);
+    std::memcpy(hb + 8 * (size_t)M, csize.data(), sizeof(uint64_t) * M);
+    CK(cudaMemcpyAsync(s.coff.p, hb, 8 * (size_t)M, cudaMemcpyHostToDevice, s.st));
+    CK(cudaMemcpyAsync(s.csize.p, hb + 8 * (size_t)M, 8 * (size_t)M, cudaMemcpyHostToDevice, s.st));
+    CK(cudaEventRecord(s.ev[2], s.st));
+    {
+        NvtxRange nr("ltgp.splice_streaming");
+        for (uint32_t w0 = 0; w0 < M; w0 += W) {  // waves in stream order
+            const uint32_t n = std::min(M, w0 + W) - w0;
+            k_splice<<<std::min<uint32_t>(n, (uint32_t)s.sms * 8), 256, 0, s.st>>>(
+                s.plans.as<PlanDev>() + w0, n, s.dir.as<DirEntry>(), s.ext.as<Extent>() + w0,
+                s.coff.as<uint64_t>() + w0, s.csize.as<uint64_t>() + w0, ts.arena.as<uint8_t>());
+            CK(cudaGetLastError());
+        }
+    }
+    CK(cudaEventRecord(s.ev[3], s.st));
+    // the children become the population, in the same arena
+    ts.version = ++g_version;
+    ts.count = M;
+    ts.h_off.assign(coff.begin(), coff.end());
+    ts.h_size.resize(M);
+    for (uint32_t c = 0; c < M; ++c) ts.h_size[c] = (uint32_t)csize[c];
+    ts.bytes = end;
+    TRY(ts.off.ensure(sizeof(uint64_t) * std::max<uint32_t>(M, 1), s.dev));
+    TRY(ts.size.ensure(sizeof(uint32_t) * std::max<uint32_t>(M, 1), s.dev));
+    CK(cudaMemcpyAsync(ts.off.p, ts.h_off.data(), sizeof(uint64_t) * M, cudaMemcpyHostToDevice, s.st));
+    CK(cudaMemcpyAsync(ts.size.p, ts.h_size.data(), sizeof(uint32_t) * M, cudaMemcpyHostToDevice, s.st));
+    s.first = 0;
+    s.count = M;
+    CK(cudaStreamSynchronize(s.st));  // the host vectors above back async copies
+    return 0;
+}
 
 int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M, ltgp_record* out,
                             int* size_limit_hit) {
@@ -1631,6 +1791,17 @@ int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M, 
                     (unsigned long long)csize[c], (unsigned long long)e->cfg.node_limit);
             return -1;
         }
+    if (e->streaming) {
+        TRY(splice_streaming(e, plans, M, csize));
+        tr.mark("splice (streaming)");
+        TRY(ltgp_evaluate_launch(e));
+        TRY(ltgp_evaluate_collect(e, out, nullptr));
+        Shard& s = e->shards[0];
+        float ms = 0.0f;
+        CK(cudaEventElapsedTime(&ms, s.ev[2], s.ev[3]));
+        e->stats.splice_seconds = ms * 1e-3;
+        return 0;
+    }
     // 4. children partitioned by bytes; splice into the other buffer
     // (parents stay readable until every shard has spliced).
     std::vector<uint32_t> old_cur(G);

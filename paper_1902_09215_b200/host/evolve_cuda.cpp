@@ -215,6 +215,7 @@ ExecOutcome execute_generation(std::span<const CrossoverPlan> plans, std::vector
         check(ltgp_upload_population(b.e, static_cast<std::uint32_t>(parents.size()), ptrs.data(), sizes.data()));
     }
     set_suite(b.e, ctx.suite);
+    if (ctx.config.streaming_memory) check(ltgp_set_streaming(b.e, 1, 0));  // evolve.hpp:45, :111-114
     std::vector<ltgp_record> rec(M);
     int flag = 0;
     check(ltgp_execute_generation(b.e, reinterpret_cast<const ltgp_plan*>(plans.data()),

@@ -247,6 +247,7 @@ ExecOutcome execute_generation(std::span<const CrossoverPlan> plans, std::vector
     std::vector<ltgp_record> rec(plans.size());
     int hit = 0;
     check(ltgp_set_memory_budget(ctx.engine, ctx.config.memory_budget_bytes));
+    if (ctx.config.streaming_memory) check(ltgp_set_streaming(ctx.engine, 1, 0));  // evolve.hpp:45
     check(ltgp_execute_generation(ctx.engine, plans.data(), static_cast<std::uint32_t>(plans.size()),
                                   rec.data(), &hit));
     if (hit == 2) return ExecOutcome{false, true};  // MemoryBudgetExceeded: nothing was built

@@ -19,6 +19,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ADD, SUB, MUL, DIV, X = 0, 1, 2, 3, 4
 
 
+def _gpus():
+    import torch
+    return torch.cuda.device_count()
+
+
 @pytest.fixture(scope="module")
 def suite():
     return ltgp.make_suite(ltgp.suite_seed(1))
@@ -631,6 +636,17 @@ def test_error_behaviour_and_edge_cases(oracle, suite):
             e.evaluate_population()
 
 
+@pytest.mark.skipif("_gpus() < 2", reason="needs >= 2 GPUs")
+def test_run_bench_cells_multi_gpu():
+    """run_bench (bench.hpp:33-35) cells with workers > 1 = GPUs
+    (driver.hpp:44-51 grid {1, 2, 4, 8}, as many as are visible)."""
+    ws = [w for w in (1, 2, 4, 8) if w <= _gpus()]
+    cells = ltgp.run_bench([1001, 100001], ws, seed=1, min_corpus_nodes=2_000_000, repeats=2)
+    assert len(cells) == 2 * len(ws)
+    assert all(c["counters_consistent"] for c in cells)
+    assert all(c["parallel_gpops"] > 0 for c in cells)
+
+
 def test_run_bench_cells():
     """run_bench (bench.hpp:33-35) on the engine: one cell per (size, GPU
     count) with consistent node counters and a positive device throughput."""
@@ -705,11 +721,6 @@ def test_depth_beyond_2_24(oracle, suite):
     assert_records_equal(rec, oracle.evaluate_population(buf, offs, sizes, suite, threads=0))
 
 
-def _gpus():
-    import torch
-    return torch.cuda.device_count()
-
-
 @pytest.mark.skipif("_gpus() < 2", reason="needs >= 2 GPUs (distinct-device NCCL all-gather and P2P splice)")
 @pytest.mark.parametrize("G", [2, 4, 8])
 def test_distinct_devices_nccl_matches_one_shard(oracle, suite, tmp_path, G):
@@ -734,5 +745,85 @@ def test_distinct_devices_nccl_matches_one_shard(oracle, suite, tmp_path, G):
     d = tmp_path / "gpu.txt"
     with ltgp.Engine(devs, node_limit=10**9) as e:
         g = e.run(400, 60, 10**9, 7, 3, str(d), 1)
+    assert g["generations"] == r["generations"] and g["nodes"] == r["nodes"]
+    assert d.read_bytes() == ref.read_bytes()
+
+
+def _streaming_model(psizes, csizes, plans, W):
+    """The engine's streaming placement (splice_streaming), restated: first
+    fit into free arena intervals, children in plan order in waves of W, a
+    parent's bytes released after the wave of its last planned use. Returns
+    (live genome high water, live byte high water)."""
+    c16 = lambda n: (int(n) + 15) // 16 * 16  # noqa: E731
+    P, M = len(psizes), len(csizes)
+    last = [-1] * P
+    for c, p in enumerate(plans):
+        last[int(p["mum_index"])] = c
+        last[int(p["dad_index"])] = c
+    live, live_b = P, sum(c16(n) for n in psizes)
+    live_hw, bytes_hw = live, live_b
+    retire = {}
+    for p in range(P):
+        retire.setdefault(0 if last[p] < 0 else last[p] // W + 1, []).append(p)
+    for p in retire.get(0, []):
+        live -= 1
+        live_b -= c16(psizes[p])
+    for w, w0 in enumerate(range(0, M, W), start=1):
+        for c in range(w0, min(M, w0 + W)):
+            live += 1
+            live_b += c16(csizes[c])
+        live_hw, bytes_hw = max(live_hw, live), max(bytes_hw, live_b)
+        for p in retire.get(w, []):
+            live -= 1
+            live_b -= c16(psizes[p])
+    return live_hw, bytes_hw
+
+
+def test_streaming_memory_mode(oracle, suite, tmp_path):
+    """RunConfig::streaming_memory (evolve.hpp:45, :111-114; SPEC.md:367,
+    :387): children spliced in waves into the parents' own
+    arena, a parent's bytes released after its last planned use. Records
+    equal the double-buffered mode's; the live-genome and live-byte high
+    waters equal a restated model of the policy and stay below 2M; a whole
+    run's dump equals the oracle's."""
+    gs = [ltgp.random_tree_of_size(300 + k, 2 * (k % 97) + 1) for k in range(500)]
+    rec0 = np.zeros(len(gs), REC)
+    with engine(suite) as e:
+        e.upload_population(gs)
+        rec0 = e.evaluate_population()
+    plans = oracle.plan_generation(9, rec0)
+    csizes = []
+    for p in plans:
+        mum, dad = gs[int(p["mum_index"])], gs[int(p["dad_index"])]
+        ms, me = oracle.subtree_extent(mum, int(p["mum_pt"]))
+        ds, de = oracle.subtree_extent(dad, int(p["dad_pt"]))
+        csizes.append(mum.size - (me - ms) + (de - ds))
+    results = {}
+    for streaming in (False, True):
+        with engine(suite) as e:
+            if streaming:
+                e.set_streaming(True, 64)
+            e.upload_population(gs)
+            e.evaluate_population()
+            rec, hit = e.execute_generation(plans)
+            assert not hit
+            st = e.stats()
+            kids = [e.download_genome(i) for i in range(0, len(gs), 37)]
+            results[streaming] = (rec, st, kids)
+    assert results[True][0].tobytes() == results[False][0].tobytes()
+    assert all(np.array_equal(a, b) for a, b in zip(results[True][2], results[False][2]))
+    live_hw, bytes_hw = _streaming_model([g.size for g in gs], csizes, plans, 64)
+    st = results[True][1]
+    assert st["live_genomes_high_water"] == live_hw < 2 * len(gs)
+    assert st["arena_used_high_water"] == bytes_hw
+    assert bytes_hw < sum((g.size + 15) // 16 * 16 for g in gs) + sum((n + 15) // 16 * 16 for n in csizes)
+    # a whole bloating run in streaming mode (arena regrows keep the parents)
+    ref = tmp_path / "ref.txt"
+    r = oracle.run(400, 60, 10**9, 7, 6, 0, str(ref), 1)
+    d = tmp_path / "gpu.txt"
+    with ltgp.Engine([0], node_limit=10**9) as e:
+        e.set_streaming(True, 32)
+        g = e.run(400, 60, 10**9, 7, 6, str(d), 1)
+        assert e.stats()["live_genomes_high_water"] < 2 * 400
     assert g["generations"] == r["generations"] and g["nodes"] == r["nodes"]
     assert d.read_bytes() == ref.read_bytes()
