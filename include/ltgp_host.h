@@ -35,6 +35,9 @@ void ltgp_host_make_suite(uint64_t seed, float* inputs48, float* targets48, floa
    the range. threads: 0 = all hardware threads. */
 uint64_t ltgp_host_corpus(uint64_t seed, uint32_t M, double lg_lo, double lg_hi, uint32_t first,
                           uint32_t count, uint8_t* buf, uint64_t* offsets, uint64_t* sizes, int threads);
+/* The host's bulk std::mt19937_64 engine against the standard library's:
+   outputs and text state (0 = identical). */
+int ltgp_host_rng_selftest(void);
 uint64_t ltgp_host_tree_seed(uint64_t seed, uint32_t i);
 /* random_tree_of_size (bench.hpp:15) from Rng(seed). 0 ok. */
 int ltgp_host_random_tree_of_size(uint64_t seed, uint64_t n, uint8_t* out);

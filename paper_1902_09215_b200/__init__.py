@@ -99,6 +99,7 @@ _HOST_SIGS = {
     "ltgp_host_corpus": (C.c_uint64, [C.c_uint64, C.c_uint32, C.c_double, C.c_double, C.c_uint32, C.c_uint32,
                                       _P, _P, _P, C.c_int]),
     "ltgp_host_tree_seed": (C.c_uint64, [C.c_uint64, C.c_uint32]),
+    "ltgp_host_rng_selftest": (C.c_int, []),
     "ltgp_host_random_tree_of_size": (C.c_int, [C.c_uint64, C.c_uint64, _P]),
     "ltgp_host_remy_tree": (C.c_int, [C.c_uint64, C.c_uint64, _P]),
     "ltgp_host_ramped": (C.c_uint64, [C.c_uint64, C.c_uint32, C.c_uint64, C.c_int, C.c_int, _P,

@@ -15,6 +15,8 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <istream>
+#include <ostream>
 #include <limits>
 #include <random>
 #include <span>
@@ -40,6 +42,71 @@ inline constexpr std::uint64_t splitmix64(std::uint64_t x) {
     x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
     return x ^ (x >> 31);
 }
+
+// The engine of rng.hpp:20-21 (std::mt19937_64) with bulk output: the
+// same recurrence, seeding and tempering as the standard's
+// mersenne_twister_engine<uint64_t, 64, 312, 156, 31, 0xb5026f5aa96619e9,
+// 29, 0x5555555555555555, 17, 0x71d67fffeda60000, 37, 0xfff7eee000000000,
+// 43, 6364136223846793005>, but each twist also tempers all 312 outputs in
+// one vectorisable pass, so a draw is a load (the standard library tempers
+// per call). Its text state is the standard's ("x0 ... x311 p"), so
+// checkpoints read and write the same form; ltgp_host_rng_selftest checks
+// outputs and text against std::mt19937_64. plan_generation is bound by
+// this stream (64K draws per 4000-child generation).
+class Mt64 {
+public:
+    static constexpr int kN = 312, kM = 156;
+    explicit Mt64(std::uint64_t s) {
+        x_[0] = s;
+        for (int i = 1; i < kN; ++i) x_[i] = 6364136223846793005ull * (x_[i - 1] ^ (x_[i - 1] >> 62)) + (std::uint64_t)i;
+        p_ = kN;
+    }
+    std::uint64_t operator()() {
+        if (p_ >= kN) refill();
+        return out_[p_++];
+    }
+    friend std::ostream& operator<<(std::ostream& os, const Mt64& m) {
+        for (int i = 0; i < kN; ++i) os << m.x_[i] << ' ';
+        return os << m.p_;
+    }
+    friend std::istream& operator>>(std::istream& is, Mt64& m) {
+        for (int i = 0; i < kN; ++i) is >> m.x_[i];
+        is >> m.p_;
+        if (is && m.p_ > (unsigned)kN) is.setstate(std::ios::failbit);
+        if (is) m.temper_all();
+        return is;
+    }
+
+private:
+    void refill() {
+        constexpr std::uint64_t kUM = ~0ull << 31, kLM = ~kUM, kA = 0xb5026f5aa96619e9ull;
+        for (int k = 0; k < kN - kM; ++k) {
+            const std::uint64_t y = (x_[k] & kUM) | (x_[k + 1] & kLM);
+            x_[k] = x_[k + kM] ^ (y >> 1) ^ ((0 - (y & 1)) & kA);
+        }
+        for (int k = kN - kM; k < kN - 1; ++k) {
+            const std::uint64_t y = (x_[k] & kUM) | (x_[k + 1] & kLM);
+            x_[k] = x_[k + kM - kN] ^ (y >> 1) ^ ((0 - (y & 1)) & kA);
+        }
+        const std::uint64_t y = (x_[kN - 1] & kUM) | (x_[0] & kLM);
+        x_[kN - 1] = x_[kM - 1] ^ (y >> 1) ^ ((0 - (y & 1)) & kA);
+        temper_all();
+        p_ = 0;
+    }
+    void temper_all() {
+        for (int i = 0; i < kN; ++i) {
+            std::uint64_t z = x_[i];
+            z ^= (z >> 29) & 0x5555555555555555ull;
+            z ^= (z << 17) & 0x71d67fffeda60000ull;
+            z ^= (z << 37) & 0xfff7eee000000000ull;
+            z ^= z >> 43;
+            out_[i] = z;
+        }
+    }
+    std::uint64_t x_[kN];
+    std::uint64_t out_[kN];
+    unsigned p_;
+};
 
 // rng.hpp:20-51: sequential stream; value mappings by hand so every output
 // is a pure function of the seed.
@@ -79,7 +146,7 @@ public:
     }
 
 private:
-    std::mt19937_64 engine_;
+    Mt64 engine_;  // std::mt19937_64's stream (rng.hpp:50)
     std::uint64_t draws_ = 0;
 };
 

@@ -15,6 +15,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <random>
+#include <sstream>
 #include <thread>
 
 #include <unistd.h>
@@ -197,17 +199,53 @@ std::size_t tournament(Rng& rng, std::span<const Individual> pop, std::uint32_t 
 // evolve.hpp:84-87. The tournaments read fitness from a
 // dense copy (4 B per individual, L1-resident) instead of the 40-byte
 // Individuals; the draws and comparisons are unchanged.
+// Selection key: an unsigned total order equal to fitness_better /
+// fitness_tied (eval.hpp:89-98): lower is better, every NaN is the worst and
+// ties every NaN, -0 ties +0. Comparing keys is branch-free, so a tournament
+// costs its RNG draws, not a mispredicted branch per entrant.
+static inline std::uint32_t selection_key(float f) {
+    if (f != f) return 0xffffffffu;
+    if (f == 0.0f) f = 0.0f;  // -0 ties +0
+    std::uint32_t b;
+    std::memcpy(&b, &f, 4);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+// tournament (evolve.hpp:79-82) on selection keys: the same draws and the
+// same winner as tournament_by(fitness_better, fitness_tied)
+static inline std::size_t tournament_keys(Rng& rng, std::uint64_t M, std::uint32_t k, const std::uint32_t* key) {
+    std::size_t best = static_cast<std::size_t>(rng.below(M));
+    std::uint32_t kb = key[best];
+    std::uint64_t ties = 1;
+    for (std::uint32_t i = 1; i < k; ++i) {
+        const std::size_t idx = static_cast<std::size_t>(rng.below(M));
+        const std::uint32_t ki = key[idx];
+        if (ki == kb) [[unlikely]] {  // tie: replace with probability 1/(ties + 1)
+            if (rng.below(ties + 1) == 0) best = idx;
+            ++ties;
+            continue;
+        }
+        const bool better = ki < kb;
+        best = better ? idx : best;
+        kb = better ? ki : kb;
+        ties = better ? 1 : ties;
+    }
+    return best;
+}
+
 std::vector<CrossoverPlan> plan_generation(Rng& rng, std::span<const Individual> pop, std::uint32_t k) {
-    std::vector<float> fit(pop.size());
-    for (std::size_t i = 0; i < pop.size(); ++i) fit[i] = pop[i].fitness;
-    const float* f = fit.data();
-    auto dense = [f](std::size_t i) { return f[i]; };
+    // dense keys and sizes: the tournaments' random reads stay in L1
+    std::vector<std::uint32_t> key(pop.size()), size(pop.size());
+    for (std::size_t i = 0; i < pop.size(); ++i) {
+        key[i] = selection_key(pop[i].fitness);
+        size[i] = pop[i].size;
+    }
     std::vector<CrossoverPlan> plans(pop.size());
     for (auto& p : plans) {
-        p.mum_index = static_cast<std::uint32_t>(tournament_by(rng, pop.size(), k, dense));
-        p.dad_index = static_cast<std::uint32_t>(tournament_by(rng, pop.size(), k, dense));
-        p.mum_pt = static_cast<std::uint32_t>(rng.below(pop[p.mum_index].size));
-        p.dad_pt = static_cast<std::uint32_t>(rng.below(pop[p.dad_index].size));
+        p.mum_index = static_cast<std::uint32_t>(tournament_keys(rng, pop.size(), k, key.data()));
+        p.dad_index = static_cast<std::uint32_t>(tournament_keys(rng, pop.size(), k, key.data()));
+        p.mum_pt = static_cast<std::uint32_t>(rng.below(size[p.mum_index]));
+        p.dad_pt = static_cast<std::uint32_t>(rng.below(size[p.dad_index]));
     }
     return plans;
 }
@@ -356,6 +394,33 @@ void ltgp_host_make_suite(uint64_t seed, float* in, float* tg, float* cs) {
     std::memcpy(in, s.inputs, sizeof s.inputs);
     std::memcpy(tg, s.targets, sizeof s.targets);
     std::memcpy(cs, s.constants, sizeof s.constants);
+}
+
+// The bulk Mt64 engine against std::mt19937_64 (the engine rng.hpp:50
+// names): outputs for several seeds across many twists, and the text state
+// both ways (a checkpoint written by one resumes in the other). 0 = equal.
+int ltgp_host_rng_selftest(void) {
+    for (const uint64_t seed : {0ull, 1ull, 42ull, 0x9e3779b97f4a7c15ull, ~0ull}) {
+        ltgp::Mt64 a(seed);
+        std::mt19937_64 b(seed);
+        for (int i = 0; i < 5000; ++i)
+            if (a() != b()) return 1;
+        std::ostringstream sa, sb;
+        sa << a;
+        sb << b;
+        if (sa.str() != sb.str()) return 2;
+        std::istringstream ia(sb.str());
+        ltgp::Mt64 c(7);
+        ia >> c;
+        std::mt19937_64 d;
+        std::istringstream ib(sa.str());
+        ib >> d;
+        for (int i = 0; i < 2000; ++i) {
+            const uint64_t x = a(), y = b(), z = c(), w = d();
+            if (x != y || x != z || x != w) return 3;
+        }
+    }
+    return 0;
 }
 
 uint64_t ltgp_host_tree_seed(uint64_t seed, uint32_t i) {

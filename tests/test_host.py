@@ -114,3 +114,9 @@ def test_run_null_out_pointers_are_errors():
     lib = ltgp.host_lib()
     assert lib.ltgp_host_run_checkpointed(None, 48, 10, 10**9, 7, 1, 1, 0, None, None, 0, None,
                                           None, None, None) == -1
+
+
+def test_bulk_mt64_engine_is_std_mt19937_64():
+    # the host's Rng engine (rng.hpp:50 names std::mt19937_64) tempers a
+    # whole twist at once; outputs and checkpoint text must be the standard's
+    assert ltgp.host_lib().ltgp_host_rng_selftest() == 0
