@@ -128,7 +128,7 @@ int ltgp_evaluate_outputs(ltgp_engine* e, ltgp_record* out, float* outs48);
 
 /* evaluate_population (evolve.hpp:108-109) on host genomes in one call:
    the packed buffer (same layout rules as ltgp_upload_packed) becomes the
-   population and is evaluated while it uploads. Slices of ~32 MB go
+   population and is evaluated while it uploads. Slices of ~16 MB go
    host-to-device on a copy stream and each slice's trees are evaluated as
    soon as they land. buf should be pinned (pageable memory works but
    serialises the copy). out: M records; outs48: per-case outputs or NULL. */

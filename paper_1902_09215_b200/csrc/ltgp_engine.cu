@@ -1155,7 +1155,11 @@ int ltgp_engine_create(const ltgp_config* cfg, ltgp_engine** out) {
     auto e = std::make_unique<ltgp_engine>();
     e->cfg = *cfg;
     if (cfg->chunk_nodes) {
-        if (cfg->chunk_nodes % 16 || cfg->chunk_nodes < 64) { set_err("chunk_nodes must be a multiple of 16 >= 64"); return -1; }
+        // <= 2^24: an item's float depth lanes stay exact (ltgp_kernels.cuh)
+        if (cfg->chunk_nodes % 16 || cfg->chunk_nodes < 64 || cfg->chunk_nodes > (1u << 24)) {
+            set_err("chunk_nodes must be a multiple of 16 in [64, 2^24]");
+            return -1;
+        }
         e->chunk = cfg->chunk_nodes;
         e->chunk_fixed = true;
     }

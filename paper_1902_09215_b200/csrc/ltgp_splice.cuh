@@ -5,8 +5,9 @@
 // count reaches zero, one warp per query, 512 opcode bytes per step.
 // k_splice replaces crossover (genome.hpp:80-84):
 // child = mum[0,ms) ++ dad[ds,de) ++ mum[me,n), one CTA per child, written as
-// aligned 32-bit words assembled with funnel shifts from the (unaligned)
-// parent bytes, which may live on a peer GPU (read over NVLink by UVA).
+// aligned 16-byte chunks assembled with funnel shifts from two aligned
+// 16-byte loads of the (unaligned) parent bytes, which may live on a peer GPU
+// (read over NVLink by UVA).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>

@@ -66,12 +66,27 @@ def main():
         print(f"cpu oracle: {k} trees x {n} nodes in {dt:.2f} s on {os.cpu_count()} threads: "
               f"{k * n * 48 / dt / 1e12:.4f} T GPops/s", flush=True)
     if a.check:
+        # every checked tree: all 48 per-case outputs and the exact record
+        # (fitness bits, hits, size, depth) against the oracle, trees checked
+        # in parallel (ctypes releases the GIL inside the oracle)
         from tests._oracle import load_oracle, same_bits
         o = load_oracle()
-        for k in range(a.check):
+
+        def check(k):
             out, _ = o.eval_batch(trees[k], suite[0], suite[2])
-            ok = same_bits(outs[k], out) and rec["depth"][k] == o.depth(trees[k])
-            print(f"tree {k}: depth {rec['depth'][k]}, matches oracle: {ok}", flush=True)
+            fit = o.fitness(out, suite[1])
+            ok = (same_bits(outs[k], out) and same_bits([rec["fitness"][k]], [fit])
+                  and rec["hits"][k] == o.hits(out, suite[1]) and rec["size"][k] == trees[k].size
+                  and rec["depth"][k] == o.depth(trees[k]))
+            return k, ok
+        t = time.perf_counter()
+        with ThreadPoolExecutor(os.cpu_count()) as ex:
+            res = list(ex.map(check, range(min(a.check, a.trees))))
+        for k, ok in res:
+            print(f"tree {k}: size {rec['size'][k]}, depth {rec['depth'][k]}, fitness {rec['fitness'][k]!r}, "
+                  f"hits {rec['hits'][k]}: matches oracle: {ok}", flush=True)
+        print(f"checked {len(res)} trees against the oracle in {time.perf_counter() - t:.1f} s: "
+              f"{sum(ok for _, ok in res)} match", flush=True)
 
 
 if __name__ == "__main__":
