@@ -17,6 +17,7 @@
 //   ref_run M G node_limit k seed grow_mode dump_path [bind_flags|default]
 #include "ltgp/evolve.hpp"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -96,7 +97,56 @@ void dump(std::FILE* f, std::uint32_t gen, const std::vector<Individual>& pop) {
 
 }  // namespace
 
+// `ref_run eval SEED COUNT`: evaluate_individual (evolve.hpp:106) and
+// eval_batch_raw / eval_batch (eval.hpp:73-79) on COUNT random genomes of the
+// suite of SEED; prints per genome: fitness bits, hits, size, depth, then the
+// 48 eval_batch_raw output bits, then whether eval_batch matched them; next
+// line: '#' + the genome in hex (the test re-evaluates it with the oracle).
+static int eval_mode(std::uint64_t seed, int count) {
+    TestSuite suite;
+    orc_make_suite(orc_suite_seed(seed), suite.inputs.data(), suite.targets.data(), suite.constants.data());
+    Rng rng(seed * 7919 + 1);
+    WorkerState worker;
+    EvalStack stack;
+    GpopsCounter counter;
+    for (int g = 0; g < count; ++g) {
+        Individual ind;
+        ind.genome = Genome(gen_tree(rng, 2 + g % 7, g % 2 == 0, 1));
+        evaluate_individual(ind, suite, worker);
+        const float* raw = eval_batch_raw(ind.genome, suite.inputs.data(), suite.constants, stack, &counter);
+        float out[kLaneWidth];  // the raw frame is valid only until the stack's next use
+        std::memcpy(out, raw, sizeof out);
+        std::uint32_t fb;
+        std::memcpy(&fb, &ind.fitness, 4);
+        std::printf("%zu %08x %d %u %u", ind.genome.size(), fb, ind.hits, ind.size, ind.depth);
+        for (std::size_t l = 0; l < kLaneWidth; ++l) {
+            std::uint32_t b;
+            std::memcpy(&b, out + l, 4);
+            std::printf(" %08x", b);
+        }
+        LaneResult in;
+        std::copy(suite.inputs.begin(), suite.inputs.end(), in.begin());
+        const LaneResult r = eval_batch(ind.genome, in, suite.constants, stack, nullptr);
+        const bool same = std::memcmp(r.data(), out, sizeof out) == 0;
+        std::printf(" %d\n", same ? 1 : 0);
+        std::printf("#");  // the genome, hex, for the test's oracle check
+        for (std::size_t k = 0; k < ind.genome.size(); ++k) std::printf("%02x", (unsigned)ind.genome[k]);
+        std::printf("\n");
+    }
+    std::printf("counter %llu %.9f peak %zu\n", (unsigned long long)counter.nodes_evaluated, counter.elapsed_seconds,
+                stack.peak_frames());
+    return 0;
+}
+
 int main(int argc, char** argv) {
+    if (argc >= 4 && std::string(argv[1]) == "eval") {
+        try {
+            return eval_mode(std::strtoull(argv[2], nullptr, 10), std::atoi(argv[3]));
+        } catch (const std::exception& ex) {
+            std::fprintf(stderr, "error: %s\n", ex.what());
+            return 6;
+        }
+    }
     if (argc < 8) {
         std::fprintf(stderr, "usage: ref_run M G node_limit k seed grow_mode dump [bind_flags|default]\n");
         return 2;

@@ -102,3 +102,32 @@ def test_reference_typed_run_size_limit(oracle, tmp_path):
     assert r["reason"] == 1 and int(out["reason"]) == 1
     assert int(out["generations"]) == r["generations"]
     assert d.read_bytes() == ref.read_bytes()
+
+
+@pytest.mark.gpu
+def test_reference_typed_single_genome_entry_points(oracle):
+    """evaluate_individual (evolve.hpp:106), eval_batch_raw and eval_batch
+    (eval.hpp:73-79) of libltgp_refabi.so, called on the reference's own
+    types (Individual, TestSuite, WorkerState, Genome, EvalStack,
+    GpopsCounter): record and all 48 outputs equal the oracle's, eval_batch
+    equals eval_batch_raw, and the GpopsCounter counts every node."""
+    import numpy as np
+    from tests._oracle import same_bits
+    r = subprocess.run([B.REF_RUN_BIN, "eval", "3", "24"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.splitlines()
+    suite = oracle.make_suite(int(oracle.orc_suite_seed(3)))
+    total = 0
+    for head, gl in zip(lines[0:-1:2], lines[1:-1:2]):
+        f = head.split()
+        g = np.frombuffer(bytes.fromhex(gl[1:]), np.uint8)
+        n, fit_bits, hits, size, depth = int(f[0]), int(f[1], 16), int(f[2]), int(f[3]), int(f[4])
+        outs = np.array([int(x, 16) for x in f[5:53]], np.uint32).view(np.float32)
+        assert f[53] == "1" and g.size == n == size
+        o, _ = oracle.eval_batch(g, suite[0], suite[2])
+        assert same_bits(outs, o)
+        assert same_bits(np.array([fit_bits], np.uint32).view(np.float32), [oracle.fitness(o, suite[1])])
+        assert hits == oracle.hits(o, suite[1]) and depth == oracle.depth(g)
+        total += n
+    counter = lines[-1].split()
+    assert counter[0] == "counter" and int(counter[1]) == total and float(counter[2]) > 0
