@@ -1491,6 +1491,9 @@ int ltgp_eval_one_record(ltgp_engine* e, const uint8_t* ops, uint64_t n, float* 
     CK(cudaMemcpyAsync(out48, s.outs.p, sizeof(float) * kLanes, cudaMemcpyDeviceToHost, s.st));
     if (rec) CK(cudaMemcpyAsync(rec, s.rec.p, sizeof(ltgp_record), cudaMemcpyDeviceToHost, s.st));
     CK(cudaStreamSynchronize(s.st));
+    float ms = 0.0f;  // device time of this evaluation (launch_eval brackets it with ev[0] / ev[1])
+    CK(cudaEventElapsedTime(&ms, s.ev[0], s.ev[1]));
+    e->stats.eval_seconds = ms * 1e-3 + s.rerun_ksecs + s.rerun_csecs;
     e->stats.nodes_evaluated += n;
     return 0;
 }
