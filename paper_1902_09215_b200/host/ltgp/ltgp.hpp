@@ -78,21 +78,10 @@ public:
     }
 
 private:
-    void refill() {
-        constexpr std::uint64_t kUM = ~0ull << 31, kLM = ~kUM, kA = 0xb5026f5aa96619e9ull;
-        for (int k = 0; k < kN - kM; ++k) {
-            const std::uint64_t y = (x_[k] & kUM) | (x_[k + 1] & kLM);
-            x_[k] = x_[k + kM] ^ (y >> 1) ^ ((0 - (y & 1)) & kA);
-        }
-        for (int k = kN - kM; k < kN - 1; ++k) {
-            const std::uint64_t y = (x_[k] & kUM) | (x_[k + 1] & kLM);
-            x_[k] = x_[k + kM - kN] ^ (y >> 1) ^ ((0 - (y & 1)) & kA);
-        }
-        const std::uint64_t y = (x_[kN - 1] & kUM) | (x_[0] & kLM);
-        x_[kN - 1] = x_[kM - 1] ^ (y >> 1) ^ ((0 - (y & 1)) & kA);
-        temper_all();
-        p_ = 0;
-    }
+    friend class Rng;
+    // the twist and the tempering of all 312 outputs (ltgp_host.cpp: one
+    // clone per vector ISA, AVX2 / AVX-512 where the host has it)
+    void refill();
     void temper_all() {
         for (int i = 0; i < kN; ++i) {
             std::uint64_t z = x_[i];
@@ -132,6 +121,50 @@ public:
         return static_cast<float>(2.0 * u - 1.0);
     }
     std::uint64_t draw_count() const { return draws_; }
+
+    // The same stream for a hot loop (plan_generation's 64K draws per
+    // generation): the stream position and the draw count live in the
+    // cursor's locals, i.e. registers. Through below() every draw is a
+    // store-to-load chain on the Rng's members (~6 ns per draw there against
+    // ~1.5 ns here). Written back when the cursor goes out of scope; the Rng
+    // must not be used directly while a cursor on it is alive.
+    class Cursor {
+    public:
+        explicit Cursor(Rng& r) : r_(r), out_(r.engine_.out_), p_(r.engine_.p_) {}
+        ~Cursor() {
+            r_.engine_.p_ = p_;
+            r_.draws_ += draws_;
+        }
+        Cursor(const Cursor&) = delete;
+        Cursor& operator=(const Cursor&) = delete;
+        std::uint64_t raw() {
+            if (p_ >= (unsigned)Mt64::kN) [[unlikely]] {
+                r_.engine_.refill();
+                p_ = 0;
+            }
+            return out_[p_++];
+        }
+        // Rng::below, draw for draw
+        std::uint64_t below(std::uint64_t n) {
+            ++draws_;
+            unsigned __int128 m = static_cast<unsigned __int128>(raw()) * n;
+            auto lo = static_cast<std::uint64_t>(m);
+            if (lo < n) [[unlikely]] {
+                const std::uint64_t threshold = (0 - n) % n;
+                while (lo < threshold) {
+                    m = static_cast<unsigned __int128>(raw()) * n;
+                    lo = static_cast<std::uint64_t>(m);
+                }
+            }
+            return static_cast<std::uint64_t>(m >> 64);
+        }
+
+    private:
+        Rng& r_;
+        const std::uint64_t* out_;
+        unsigned p_;
+        std::uint64_t draws_ = 0;
+    };
     // Checkpoint/resume: the engine state in the
     // standard's portable text form, then the draw counter.
     std::string state() const {
