@@ -154,6 +154,17 @@ int ltgp_evaluate_collect(ltgp_engine* e, ltgp_record* out, uint64_t* nodes);
 int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M,
                             ltgp_record* out, int* size_limit_hit);
 
+/* ltgp_execute_generation in two halves, so the caller's host work overlaps
+   the device's: launch validates the plans and, on a single-shard
+   double-buffered engine, issues the whole generation (one CUDA graph:
+   directory, extents, child layout and limit checks, work list, splice,
+   evaluation, readback) without waiting; finish waits once and reports
+   exactly what ltgp_execute_generation reports. No other call on the engine
+   between the two. (Multi-shard and streaming engines run the generation
+   inside finish.) */
+int ltgp_execute_generation_launch(ltgp_engine* e, const ltgp_plan* plans, uint32_t M);
+int ltgp_execute_generation_finish(ltgp_engine* e, ltgp_record* out, int* size_limit_hit);
+
 /* Generation statistics of the current population (after an evaluation or
    execute_generation): no host pass over the records. */
 int ltgp_generation_stats(ltgp_engine* e, ltgp_gen_stats* out);

@@ -83,6 +83,8 @@ _CUDA_SIGS = {
     "ltgp_evaluate_launch": (C.c_int, [_P]),
     "ltgp_evaluate_collect": (C.c_int, [_P, _P, _P]),
     "ltgp_execute_generation": (C.c_int, [_P, _P, C.c_uint32, _P, C.POINTER(C.c_int)]),
+    "ltgp_execute_generation_launch": (C.c_int, [_P, _P, C.c_uint32]),
+    "ltgp_execute_generation_finish": (C.c_int, [_P, _P, C.POINTER(C.c_int)]),
     "ltgp_download_genome": (C.c_int, [_P, C.c_uint32, _P, C.c_uint64, C.POINTER(C.c_uint64)]),
     "ltgp_eval_one": (C.c_int, [_P, _P, C.c_uint64, _P]),
     "ltgp_eval_one_record": (C.c_int, [_P, _P, C.c_uint64, _P, _P]),
@@ -390,6 +392,21 @@ class Engine:
         hit = C.c_int()
         _check(self._lib.ltgp_execute_generation(self._h, _ptr(plans), len(plans), _ptr(rec), C.byref(hit)))
         return rec, bool(hit.value)
+
+    def execute_generation_launch(self, plans: np.ndarray):
+        """First half of execute_generation: issues the generation, returns
+        without waiting (see ltgp_execute_generation_launch)."""
+        self._pending_plans = np.ascontiguousarray(plans, PLAN_DTYPE)
+        _check(self._lib.ltgp_execute_generation_launch(self._h, _ptr(self._pending_plans),
+                                                        len(self._pending_plans)))
+
+    def execute_generation_finish(self):
+        """Second half: waits; returns (records, outcome) with outcome 0,
+        1 = SizeLimitHit or 2 = MemoryBudgetExceeded."""
+        rec = np.zeros(len(self._pending_plans), RECORD_DTYPE)
+        hit = C.c_int()
+        _check(self._lib.ltgp_execute_generation_finish(self._h, _ptr(rec), C.byref(hit)))
+        return rec, int(hit.value)
 
     def download_genome(self, idx: int) -> np.ndarray:
         n = C.c_uint64()

@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "../../include/ltgp_cuda.h"
+#include "ltgp_gen.cuh"
 #include "ltgp_kernels.cuh"
 #include "ltgp_splice.cuh"
 
@@ -254,6 +255,19 @@ struct Shard {
     HostBuf h_csize, h_coff, h_dir;
     DevBuf gstats;      // generation statistics scratch (GenStatsDev + best bits)
     HostBuf h_gstats;
+    // device-resident generation (execute_generation_device): its status,
+    // per-child work-list scratch, pinned staging (plans in; status,
+    // counters, records and the children's layout out) and one captured
+    // CUDA graph per parity of s.cur, re-captured when an argument changes
+    DevBuf gen_status, gen_tree;
+    HostBuf h_gen;
+    cudaGraphExec_t gen_exec[2] = {};
+    std::vector<uint8_t> gen_sig[2];
+    struct GenPending {  // a launched device generation, until its finish
+        size_t o_st = 0, o_cnt = 0, o_rec = 0, o_off = 0, o_size = 0;  // staging offsets
+        EvalArgs a{};
+        CombineArgs ca{};
+    } genp;
     void release() {
         set[0].release(); set[1].release(); scratch.release();
         for (DevBuf* b : {&items, &ctrees, &hdr, &steps, &frames, &dframes, &segs, &spill, &counters,
@@ -262,6 +276,8 @@ struct Shard {
                           &rerun_slot[1], &ovf, &big_spill, &gstats, &runs, &cch, &cres, &saddr, &big_addr[0],
                           &big_addr[1]}) b->release();
         h_gstats.release();
+        gen_status.release(); gen_tree.release(); h_gen.release();
+        for (auto& g : gen_exec) if (g) cudaGraphExecDestroy(g);
         h_items.release(); h_ctrees.release(); h_counters.release();
         h_csize.release(); h_coff.release(); h_dir.release();
         for (auto& b : xspill) b.release();
@@ -295,6 +311,12 @@ struct ltgp_engine {
     uint64_t used_high_water = 0;    // arena bytes holding live genomes
     ltgp_stats stats;
     HostBuf staging;
+    // ltgp_execute_generation_launch .. _finish
+    struct Pending {
+        bool active = false, device = false;
+        uint32_t M = 0;
+        std::vector<ltgp_plan> plans;  // host path: the plans, run at finish
+    } pend;
     // record all-gather of a multi-shard population: every
     // shard's records into one n_shards x cmax array on each device
     struct Gather {
@@ -607,6 +629,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     a.size = ts.size.as<uint32_t>();
     a.items = s.items.as<Item>();
     a.n_items = nitems;
+    a.n_items_dev = nullptr;
     a.counters = s.counters.as<uint32_t>();
     a.queue = s.counters.as<uint32_t>();
     a.item_base = 0;
@@ -639,6 +662,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     ca.rec = s.rec.as<float>();
     ca.outs = a.outs;
     ca.counters = s.counters.as<uint32_t>();
+    ca.counts_dev = nullptr;
     s.last_outs = want_outs;
     s.last_reruns = 0;
     s.rerun_ksecs = s.rerun_csecs = 0.0;
@@ -695,14 +719,14 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             ++launches;
         }
         if (ni && fuse_decode) {  // a warp per item, decoding as it plans
-            k_plan_warp<true><<<(ni + 3) / 4, 128, 0, X>>>(s.items.as<Item>() + i0, ni, ts.off.as<uint64_t>(),
+            k_plan_warp<true><<<(ni + 3) / 4, 128, 0, X>>>(s.items.as<Item>() + i0, ni, nullptr, ts.off.as<uint64_t>(),
                                                           reinterpret_cast<uint8_t*>(dec), ts.meta.as<uint32_t>(),
                                                           ts.arena.as<uint4>(), packets, kWindow, pool);
             CK(cudaGetLastError());
             DEBUG_SYNC(X, "k_plan_warp");
             ++launches;
         } else if (ni && plan_warp) {  // a warp per item, after k_decode
-            k_plan_warp<false><<<(ni + 3) / 4, 128, 0, X>>>(s.items.as<Item>() + i0, ni, ts.off.as<uint64_t>(),
+            k_plan_warp<false><<<(ni + 3) / 4, 128, 0, X>>>(s.items.as<Item>() + i0, ni, nullptr, ts.off.as<uint64_t>(),
                                                            reinterpret_cast<uint8_t*>(dec), ts.meta.as<uint32_t>(),
                                                            ts.arena.as<uint4>(), packets, kWindow, pool);
             CK(cudaGetLastError());
@@ -1695,7 +1719,7 @@ static int splice_streaming(ltgp_engine* e, const ltgp_plan* plans, uint32_t M, 
             const uint32_t n = std::min(M, w0 + W) - w0;
             k_splice<<<std::min<uint32_t>(n, (uint32_t)s.sms * 8), 256, 0, s.st>>>(
                 s.plans.as<PlanDev>() + w0, n, s.dir.as<DirEntry>(), s.ext.as<Extent>() + w0,
-                s.coff.as<uint64_t>() + w0, s.csize.as<uint64_t>() + w0, ts.arena.as<uint8_t>());
+                s.coff.as<uint64_t>() + w0, s.csize.as<uint64_t>() + w0, ts.arena.as<uint8_t>(), nullptr);
             CK(cudaGetLastError());
         }
     }
@@ -1717,17 +1741,358 @@ static int splice_streaming(ltgp_engine* e, const ltgp_plan* plans, uint32_t M, 
     return 0;
 }
 
-int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M, ltgp_record* out,
-                            int* size_limit_hit) {
-    if (!e || !plans || !size_limit_hit) { set_err("null argument"); return -1; }
-    if (M != e->M) { set_err("plan count %u != population size %u", M, e->M); return -1; }
-    if (!e->have_suite) { set_err("ltgp_set_suite not called"); return -1; }
-    *size_limit_hit = 0;
-    for (uint32_t c = 0; c < M; ++c)
-        if (plans[c].mum_index >= M || plans[c].dad_index >= M) {
-            set_err("plan %u references slot outside the population", c);
-            return -1;
+// Device-resident generation:
+// single shard, double-buffered. One launch sequence on s.st, captured as a
+// CUDA graph (one per parity of s.cur; LTGP_GEN_GRAPH=0: plain launches):
+//   plans H2D -> k_gen_dir -> k_extent -> k_gen_control (child sizes,
+//   layout, budget / size-limit / capacity checks, chunk length, work-list
+//   bases) -> k_gen_items -> k_splice -> k_plan_warp -> k_eval -> k_cpops ->
+//   k_caddr -> k_combine -> status, counters, records and the children's
+//   layout D2H
+// and one synchronisation. Every kernel after k_gen_control reads its counts
+// (or its skip word) from the device status, so a generation that hits a
+// limit splices and evaluates nothing. Capacities are grow-only buffers
+// sized from the previous generation; a generation that outgrows the
+// children's arena returns 1 (the host path runs it, growing the arena); one
+// whose work list outgrows its buffers is evaluated by the host path's
+// launch_eval after the device splice.
+static bool gen_graph_enabled() {
+    static const bool v = !(std::getenv("LTGP_GEN_GRAPH") && std::atoi(std::getenv("LTGP_GEN_GRAPH")) == 0);
+    return v;
+}
+static bool device_generation_enabled() {
+    static const bool v = !(std::getenv("LTGP_DEVICE_GEN") && std::atoi(std::getenv("LTGP_DEVICE_GEN")) == 0);
+    return v;
+}
+
+static int gen_device_launch(ltgp_engine* e, const ltgp_plan* plans, uint32_t M) {
+    Trace tr("ltgp.execute_generation_device");
+    Shard& s = e->shards[0];
+    TreeSet& par = s.set[s.cur];
+    TreeSet& ch = s.set[1 - s.cur];
+    CK(cudaSetDevice(s.dev));
+    // --- capacities (grow-only; estimates from the parents and the last evaluation)
+    TRY(ch.arena.ensure(std::max<uint64_t>(par.bytes + par.bytes / 4, 4096) + 64, s.dev));
+    TRY(ch.off.ensure(sizeof(uint64_t) * M, s.dev));
+    TRY(ch.size.ensure(sizeof(uint32_t) * M, s.dev));
+    const uint64_t packets = ch.arena.bytes / 16;
+    TRY(ch.decode.ensure(packets * 32 + 1024, s.dev));
+    TRY(ch.meta.ensure(64, s.dev));  // k_plan_warp<true> decodes itself: no metadata pass
+    TRY(s.plans.ensure(sizeof(PlanDev) * M, s.dev));
+    TRY(s.ext.ensure(sizeof(Extent) * M, s.dev));
+    TRY(s.csize.ensure(sizeof(uint64_t) * M, s.dev));
+    TRY(s.dir.ensure(sizeof(DirEntry) * M, s.dev));
+    TRY(s.gen_status.ensure(sizeof(GenStatus), s.dev));
+    TRY(s.gen_tree.ensure(sizeof(uint32_t) * 2 * M, s.dev));
+    TRY(s.items.ensure(sizeof(Item) * ((uint64_t)s.last_items + s.last_items / 2 + M + 1024), s.dev));
+    const uint32_t items_cap = (uint32_t)std::min<uint64_t>(s.items.bytes / sizeof(Item), 0xffffffffu);
+    TRY(s.ovf.ensure(sizeof(uint32_t) * items_cap, s.dev));
+    const uint64_t chunks_want = (uint64_t)s.last_chunks + s.last_chunks / 2 + 1024;
+    TRY(s.hdr.ensure(sizeof(ChunkHdr) * chunks_want, s.dev));
+    TRY(s.dframes.ensure((size_t)kFrameBytes * chunks_want, s.dev));
+    TRY(s.segs.ensure(sizeof(Seg) * 2 * chunks_want, s.dev));
+    TRY(s.runs.ensure(sizeof(PopRun) * 3 * chunks_want, s.dev));
+    TRY(s.cch.ensure(sizeof(CombChunk) * chunks_want, s.dev));
+    const uint32_t chunks_cap = (uint32_t)std::min<uint64_t>(
+        {s.hdr.bytes / sizeof(ChunkHdr), s.dframes.bytes / kFrameBytes, s.segs.bytes / (2 * sizeof(Seg)),
+         s.runs.bytes / (3 * sizeof(PopRun)), s.cch.bytes / sizeof(CombChunk), 0xffffffffull});
+    TRY(s.ctrees.ensure(sizeof(CombineTree) * M, s.dev));
+    TRY(s.cres.ensure(sizeof(CombResult) * M, s.dev));
+    {   // chunk-summary pool: launch_eval's estimate at the last chunk length
+        const double rc = std::sqrt((double)s.cur_chunk);
+        const double pf = std::max(std::min(2.0 * rc, (double)s.cur_chunk + 2), s.pool_per_chunk_f * 1.25);
+        const double ps = std::max(std::min(2.0 * rc, (double)s.cur_chunk), s.pool_per_chunk_s * 1.25);
+        TRY(s.frames.ensure((size_t)((pf * chunks_want + 64) * kFrameBytes), s.dev));
+        TRY(s.steps.ensure((size_t)(ps * chunks_want + 1024), s.dev));
+        TRY(s.saddr.ensure(s.steps.bytes * 8, s.dev));
+    }
+    TRY(s.rec.ensure(sizeof(ltgp_record) * M, s.dev));
+    const uint32_t sf = spill_frames(s.cur_chunk);
+    TRY(s.spill.ensure((size_t)s.eval_grid * kWarps * sf * kFrameBytes, s.dev));
+    // pinned staging: plans | status | counters | records | child offsets | child sizes
+    const size_t o_st = (sizeof(PlanDev) * M + 255) & ~size_t(255);
+    const size_t o_cnt = o_st + ((sizeof(GenStatus) + 255) & ~size_t(255));
+    const size_t o_rec = o_cnt + 256;
+    const size_t o_off = o_rec + sizeof(ltgp_record) * M;
+    const size_t o_size = o_off + sizeof(uint64_t) * M;
+    TRY(s.h_gen.ensure(o_size + sizeof(uint32_t) * M));
+    uint8_t* hg = s.h_gen.as<uint8_t>();
+    tr.mark("capacities");
+    // --- arguments
+    GenStatus* st = s.gen_status.as<GenStatus>();
+    GenArgs ga{};
+    ga.plans = s.plans.as<PlanDev>();
+    ga.dir = s.dir.as<DirEntry>();
+    ga.ext = s.ext.as<Extent>();
+    ga.ext_err = s.counters.as<uint32_t>() + 3;
+    ga.M = M;
+    ga.node_limit = e->cfg.node_limit;
+    ga.budget = e->memory_budget;
+    ga.arena_cap = ch.arena.bytes;
+    ga.csize = s.csize.as<uint64_t>();
+    ga.child_off = ch.off.as<uint64_t>();
+    ga.child_size = ch.size.as<uint32_t>();
+    ga.tree_chunk0 = s.gen_tree.as<uint32_t>();
+    ga.tree_ct = s.gen_tree.as<uint32_t>() + M;
+    ga.items = s.items.as<Item>();
+    ga.items_cap = items_cap;
+    ga.ctrees = s.ctrees.as<CombineTree>();
+    ga.chunks_cap = chunks_cap;
+    ga.fixed_chunk = e->chunk_fixed ? e->chunk : 0u;
+    ga.default_chunk = kDefaultChunk;
+    ga.max_chunk = kMaxChunk;
+    ga.grid_warps = (uint32_t)s.eval_grid * kWarps;
+    ga.st = st;
+    PlanPool pool{};
+    pool.hdr = s.hdr.as<ChunkHdr>();
+    pool.frames = s.frames.as<float2>();
+    pool.steps = s.steps.as<uint8_t>();
+    pool.used = reinterpret_cast<unsigned long long*>(s.counters.as<uint32_t>() + kPoolCounters);
+    pool.cap_frames = s.frames.bytes / kFrameBytes;
+    pool.cap_steps = s.steps.bytes;
+    pool.spill_frames = sf;
+    pool.adjusts = s.counters.as<uint32_t>() + 5;
+    pool.flags = s.counters.as<uint32_t>() + 1;
+    EvalArgs a{};
+    a.arena = ch.arena.as<uint8_t>();
+    a.decode = ch.decode.as<uint4>();
+    a.off = ch.off.as<uint64_t>();
+    a.size = ch.size.as<uint32_t>();
+    a.items = s.items.as<Item>();
+    a.n_items = 0;
+    a.n_items_dev = &st->n_items;
+    a.counters = s.counters.as<uint32_t>();
+    a.hdr = s.hdr.as<ChunkHdr>();
+    a.steps = s.steps.as<uint8_t>();
+    a.frames = s.frames.as<float2>();
+    a.max_steps = 0xffffffffu;
+    a.max_frames = 0xffffffffu;
+    a.spill = s.spill.as<float2>();
+    a.spill_frames = sf;
+    a.rec = s.rec.as<float>();
+    a.outs = nullptr;
+    a.slot = nullptr;
+    a.packets = packets;
+    a.ovf = s.ovf.as<uint32_t>();
+    a.queue = s.counters.as<uint32_t>();
+    a.item_base = 0;
+    CombineArgs ca{};
+    ca.trees = s.ctrees.as<CombineTree>();
+    ca.counts_dev = &st->n_trees;
+    ca.hdr = s.hdr.as<ChunkHdr>();
+    ca.chunk0 = 0;
+    ca.dframes = s.dframes.as<float2>();
+    ca.segs = s.segs.as<Seg>();
+    ca.runs = s.runs.as<PopRun>();
+    ca.cch = s.cch.as<CombChunk>();
+    ca.cres = s.cres.as<CombResult>();
+    ca.space[0] = StepSpace{s.steps.as<uint8_t>(), pool.cap_steps, s.saddr.as<uint64_t>()};
+    ca.space[1] = ca.space[2] = StepSpace{nullptr, 0, nullptr};
+    ca.rec = s.rec.as<float>();
+    ca.outs = nullptr;
+    ca.counters = s.counters.as<uint32_t>();
+    const uint32_t seg_cap = kCpopsSmem / (uint32_t)sizeof(Seg);
+    const unsigned plan_blocks = (items_cap + 3) / 4;
+    const unsigned cblocks = std::min<unsigned>((M + kCombineWarps - 1) / kCombineWarps, (unsigned)s.sms * 16);
+    const unsigned ablocks = (unsigned)s.sms * 16;
+    // --- the launch sequence (recorded into a graph, or issued directly)
+    const bool graph = gen_graph_enabled();
+    auto record = [&](cudaEvent_t ev) {
+        return graph ? cudaEventRecordWithFlags(ev, s.st, cudaEventRecordExternal) : cudaEventRecord(ev, s.st);
+    };
+    auto issue = [&]() -> int {
+        CK(cudaMemcpyAsync(s.plans.p, hg, sizeof(PlanDev) * M, cudaMemcpyHostToDevice, s.st));
+        CK(cudaMemsetAsync(s.counters.p, 0, kCounterBytes, s.st));
+        k_gen_dir<<<(M + 255) / 256, 256, 0, s.st>>>(par.arena.as<uint8_t>(), par.off.as<uint64_t>(),
+                                                     par.size.as<uint32_t>(), M, s.dir.as<DirEntry>());
+        CK(cudaGetLastError());
+        k_extent<<<(2 * M + 3) / 4, 128, 0, s.st>>>(s.plans.as<PlanDev>(), M, s.dir.as<DirEntry>(), s.ext.as<Extent>(),
+                                                  nullptr, s.counters.as<uint32_t>() + 3);
+        CK(cudaGetLastError());
+        k_gen_control<<<1, 1024, 0, s.st>>>(ga);
+        CK(cudaGetLastError());
+        k_gen_items<<<(M + 7) / 8, 256, 0, s.st>>>(ga);
+        CK(cudaGetLastError());
+        CK(record(s.ev[2]));
+        k_splice<<<std::min<uint32_t>(M, (uint32_t)s.sms * 8), 256, 0, s.st>>>(
+            s.plans.as<PlanDev>(), M, s.dir.as<DirEntry>(), s.ext.as<Extent>(), ch.off.as<uint64_t>(),
+            s.csize.as<uint64_t>(), ch.arena.as<uint8_t>(), &st->fatal);
+        CK(cudaGetLastError());
+        CK(record(s.ev[3]));
+        CK(record(s.ev[0]));
+        k_plan_warp<true><<<plan_blocks, 128, 0, s.st>>>(s.items.as<Item>(), 0u, &st->n_items, ch.off.as<uint64_t>(),
+                                                         reinterpret_cast<uint8_t*>(ch.decode.p), ch.meta.as<uint32_t>(),
+                                                         ch.arena.as<uint4>(), packets, kWindow, pool);
+        CK(cudaGetLastError());
+        CK(record(s.kev[0]));
+        K_EVAL<<<s.eval_grid, kWarps * 32, eval_smem_bytes(), s.st>>>(a, e->suite);
+        CK(cudaGetLastError());
+        CK(record(s.kev[1]));
+        CK(record(s.ev[4]));
+        k_cpops<<<M, 32, seg_cap * sizeof(Seg), s.st>>>(ca, seg_cap);
+        CK(cudaGetLastError());
+        k_caddr<<<ablocks, 128, 0, s.st>>>(ca);
+        CK(cudaGetLastError());
+        k_combine<<<cblocks, kCombineWarps * 32, 0, s.st>>>(ca, e->suite);
+        CK(cudaGetLastError());
+        CK(record(s.ev[1]));
+        CK(cudaMemcpyAsync(hg + o_st, st, sizeof(GenStatus), cudaMemcpyDeviceToHost, s.st));
+        CK(cudaMemcpyAsync(hg + o_cnt, s.counters.p, 64, cudaMemcpyDeviceToHost, s.st));
+        CK(cudaMemcpyAsync(hg + o_rec, s.rec.p, sizeof(ltgp_record) * M, cudaMemcpyDeviceToHost, s.st));
+        CK(cudaMemcpyAsync(hg + o_off, ch.off.p, sizeof(uint64_t) * M, cudaMemcpyDeviceToHost, s.st));
+        CK(cudaMemcpyAsync(hg + o_size, ch.size.p, sizeof(uint32_t) * M, cudaMemcpyDeviceToHost, s.st));
+        return 0;
+    };
+    std::memcpy(hg, plans, sizeof(PlanDev) * M);
+    tr.mark("arguments");
+    if (graph) {
+        // the graph bakes in every argument: re-capture when one changes
+        std::vector<uint8_t> sig;
+        auto add = [&](const void* p, size_t n) {
+            const uint8_t* b = static_cast<const uint8_t*>(p);
+            sig.insert(sig.end(), b, b + n);
+        };
+        const void* ptrs[] = {par.arena.p, par.off.p, par.size.p, hg, s.spill.p};
+        add(&ga, sizeof ga); add(&pool, sizeof pool); add(&a, sizeof a); add(&ca, sizeof ca);
+        add(&e->suite, sizeof e->suite); add(ptrs, sizeof ptrs); add(&s.eval_grid, sizeof s.eval_grid);
+        cudaGraphExec_t& ex = s.gen_exec[s.cur];
+        if (!ex || s.gen_sig[s.cur] != sig) {
+            if (ex) { cudaGraphExecDestroy(ex); ex = nullptr; }
+            cudaGraph_t g = nullptr;
+            CK(cudaStreamBeginCapture(s.st, cudaStreamCaptureModeThreadLocal));
+            const int r = issue();
+            const cudaError_t ce = cudaStreamEndCapture(s.st, &g);
+            if (r != 0) { if (g) cudaGraphDestroy(g); return -1; }
+            CK(ce);
+            const cudaError_t ie = cudaGraphInstantiate(&ex, g, 0);
+            cudaGraphDestroy(g);
+            CK(ie);
+            s.gen_sig[s.cur] = std::move(sig);
+            tr.mark("capture");
         }
+        CK(cudaGraphLaunch(ex, s.st));
+    } else {
+        TRY(issue());
+    }
+    auto& gp = s.genp;
+    gp.o_st = o_st; gp.o_cnt = o_cnt; gp.o_rec = o_rec; gp.o_off = o_off; gp.o_size = o_size;
+    gp.a = a;
+    gp.ca = ca;
+    tr.mark("launch");
+    return 0;
+}
+
+// The launched generation's outcome (after one synchronisation). Returns 1
+// when the host path must run the generation instead (arena grown).
+static int gen_device_finish(ltgp_engine* e, uint32_t M, ltgp_record* out, int* size_limit_hit) {
+    Trace tr("ltgp.execute_generation_device");
+    Shard& s = e->shards[0];
+    TreeSet& ch = s.set[1 - s.cur];
+    CK(cudaSetDevice(s.dev));
+    CK(cudaStreamSynchronize(s.st));
+    tr.mark("sync");
+    const auto& gp = s.genp;
+    const size_t o_st = gp.o_st, o_cnt = gp.o_cnt, o_rec = gp.o_rec, o_off = gp.o_off, o_size = gp.o_size;
+    const EvalArgs& a = gp.a;
+    const CombineArgs& ca = gp.ca;
+    const uint8_t* hg = s.h_gen.as<uint8_t>();
+    // --- outcome
+    const GenStatus g = *reinterpret_cast<const GenStatus*>(hg + o_st);
+    std::memcpy(s.h_counters.p, hg + o_cnt, 64);
+    if (g.fatal & 32u) { set_err("malformed parent genome in extent scan"); return -1; }
+    if (g.fatal & 2u) { *size_limit_hit = 2; return 0; }  // MemoryBudgetExceeded: nothing was built
+    if (g.fatal & 1u) { *size_limit_hit = 1; return 0; }  // SizeLimitHit
+    if (g.fatal & 4u) {
+        set_err("child of %llu nodes: beyond the engine's 2^32-1-node tree capacity (node_limit %llu)",
+                (unsigned long long)g.max_child, (unsigned long long)e->cfg.node_limit);
+        return -1;
+    }
+    if (g.fatal & 8u) {  // the children need a larger arena: grow it, the host path runs this generation
+        TRY(ch.arena.ensure(g.child_bytes + 64, s.dev));
+        return 1;
+    }
+    // the children (spliced) become the population
+    ch.version = ++g_version;
+    ch.count = M;
+    ch.h_off.assign(reinterpret_cast<const uint64_t*>(hg + o_off), reinterpret_cast<const uint64_t*>(hg + o_off) + M);
+    ch.h_size.assign(reinterpret_cast<const uint32_t*>(hg + o_size),
+                     reinterpret_cast<const uint32_t*>(hg + o_size) + M);
+    ch.bytes = g.child_bytes;
+    s.cur = 1 - s.cur;
+    s.first = 0;
+    s.count = M;
+    s.items_for = nullptr;  // the host work-list cache does not describe these items
+    float ms = 0.0f;
+    CK(cudaEventElapsedTime(&ms, s.ev[2], s.ev[3]));
+    const double splice_s = ms * 1e-3;
+    if (g.flags & 16u) {  // work list beyond its buffers: the host path evaluates (and grows them)
+        TRY(ltgp_evaluate_launch(e));
+        TRY(ltgp_evaluate_collect(e, out, nullptr));
+        e->stats.splice_seconds = splice_s;
+        return 0;
+    }
+    const uint32_t C = g.chunk;
+    const uint32_t rc = (uint32_t)std::lround(std::sqrt((double)C));
+    s.cur_chunk = C;
+    s.cur_max_frames = std::max<uint32_t>(kMaxFrames, (6 * rc + 63) & ~63u);
+    s.cur_max_steps = std::min<uint32_t>(C, std::max<uint32_t>(kMaxSteps, 16 * rc));
+    s.last_items = g.n_items;
+    s.last_chunks = g.n_chunks;
+    s.last_ctrees = g.n_trees;
+    s.max_tree_chunks = g.max_chunks;
+    s.eargs = a;  // for the overflow re-runs: the counts on the host
+    s.eargs.n_items = g.n_items;
+    s.eargs.n_items_dev = nullptr;
+    s.cargs = ca;
+    s.cargs.n_trees = g.n_trees;
+    s.cargs.n_chunks = g.n_chunks;
+    s.cargs.counts_dev = nullptr;
+    s.last_outs = false;
+    s.last_reruns = 0;
+    s.rerun_ksecs = s.rerun_csecs = 0.0;
+    const uint32_t* hc = s.h_counters.as<uint32_t>();
+    const bool reruns = hc[2] != 0;
+    if (reruns) {  // rerun_overflowed reads the work list from s.h_items
+        TRY(s.h_items.ensure(sizeof(Item) * std::max<uint32_t>(g.n_items, 1)));
+        CK(cudaMemcpyAsync(s.h_items.p, s.items.p, sizeof(Item) * g.n_items, cudaMemcpyDeviceToHost, s.st));
+        CK(cudaStreamSynchronize(s.st));
+    }
+    TRY(finish_eval(e, s));
+    if (out) {
+        if (reruns) {
+            CK(cudaMemcpyAsync(out, s.rec.p, sizeof(ltgp_record) * M, cudaMemcpyDeviceToHost, s.st));
+            CK(cudaStreamSynchronize(s.st));
+        } else {
+            std::memcpy(out, hg + o_rec, sizeof(ltgp_record) * M);
+        }
+    }
+    CK(cudaEventElapsedTime(&ms, s.ev[0], s.ev[4]));
+    const double k = ms * 1e-3 + s.rerun_ksecs;
+    CK(cudaEventElapsedTime(&ms, s.ev[4], s.ev[1]));
+    const double cmb = ms * 1e-3 + s.rerun_csecs;
+    CK(cudaEventElapsedTime(&ms, s.kev[0], s.kev[1]));
+    e->stats.keval_seconds = ms * 1e-3;
+    e->stats.eval_seconds = k + cmb;
+    e->stats.eval_kernel_seconds = k;
+    e->stats.combine_seconds = cmb;
+    e->stats.splice_seconds = splice_s;
+    e->stats.nodes_evaluated += g.nodes;
+    e->stats.last_chunks = g.n_chunks;
+    e->stats.last_spine_steps = s.last_steps;
+    e->stats.last_exits = hc[4];
+    e->stats.last_window_adjusts = hc[5];
+    e->stats.last_fallback_items = s.last_reruns;
+    e->stats.kernel_launches = 10;
+    s.kev_valid = true;
+    tr.mark("finish");
+    return 0;
+}
+
+// The host-orchestrated generation (multi-shard and streaming engines, and
+// the device path's fallback): directory, extents, limit checks and layout
+// on the host, kernels per phase.
+static int execute_generation_host(ltgp_engine* e, const ltgp_plan* plans, uint32_t M, ltgp_record* out,
+                                   int* size_limit_hit) {
     Trace tr("ltgp.execute_generation");
     std::vector<DirEntry> dir;
     build_directory(e, dir);
@@ -1842,7 +2207,7 @@ int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M, 
         NvtxRange nr_splice("ltgp.splice");
         k_splice<<<std::min<uint32_t>(s.count, (uint32_t)s.sms * 8), 256, 0, s.st>>>(
             s.plans.as<PlanDev>(), s.count, s.dir.as<DirEntry>(), s.ext.as<Extent>(), s.coff.as<uint64_t>(),
-            s.csize.as<uint64_t>(), ts.arena.as<uint8_t>());
+            s.csize.as<uint64_t>(), ts.arena.as<uint8_t>(), nullptr);
         CK(cudaGetLastError());
         CK(cudaEventRecord(s.ev[3], s.st));
         CK(cudaMemcpyAsync(ts.off.p, ts.h_off.data(), sizeof(uint64_t) * ts.count, cudaMemcpyHostToDevice, s.st));
@@ -1867,6 +2232,57 @@ int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M, 
     e->stats.splice_seconds = splice_ms * 1e-3;
     tr.mark("eval collect");
     return 0;
+}
+
+int ltgp_execute_generation_launch(ltgp_engine* e, const ltgp_plan* plans, uint32_t M) {
+    if (!e || !plans) { set_err("null argument"); return -1; }
+    if (e->pend.active) { set_err("the launched generation is not finished (ltgp_execute_generation_finish)"); return -1; }
+    if (M != e->M) { set_err("plan count %u != population size %u", M, e->M); return -1; }
+    if (!e->have_suite) { set_err("ltgp_set_suite not called"); return -1; }
+    for (uint32_t c = 0; c < M; ++c)
+        if (plans[c].mum_index >= M || plans[c].dad_index >= M) {
+            set_err("plan %u references slot outside the population", c);
+            return -1;
+        }
+    auto& p = e->pend;
+    p.M = M;
+    p.device = e->shards.size() == 1 && !e->streaming && device_generation_enabled();
+    if (p.device) {
+        const TreeSet& par = e->shards[0].set[e->shards[0].cur];
+        for (uint32_t c = 0; c < M; ++c)
+            if (plans[c].mum_pt >= par.h_size[plans[c].mum_index] || plans[c].dad_pt >= par.h_size[plans[c].dad_index]) {
+                set_err("plan %u: crossover point out of range", c);  // std::out_of_range
+                return -1;
+            }
+        TRY(gen_device_launch(e, plans, M));
+    } else {
+        p.plans.assign(plans, plans + M);
+    }
+    p.active = true;
+    return 0;
+}
+
+int ltgp_execute_generation_finish(ltgp_engine* e, ltgp_record* out, int* size_limit_hit) {
+    if (!e || !size_limit_hit) { set_err("null argument"); return -1; }
+    auto& p = e->pend;
+    if (!p.active) { set_err("no launched generation (ltgp_execute_generation_launch)"); return -1; }
+    p.active = false;
+    *size_limit_hit = 0;
+    if (p.device) {
+        const int r = gen_device_finish(e, p.M, out, size_limit_hit);
+        if (r <= 0) return r;
+        // the children's arena was grown: the host path runs this generation
+        p.plans.resize(p.M);
+        std::memcpy(p.plans.data(), e->shards[0].h_gen.p, sizeof(ltgp_plan) * p.M);
+    }
+    return execute_generation_host(e, p.plans.data(), p.M, out, size_limit_hit);
+}
+
+int ltgp_execute_generation(ltgp_engine* e, const ltgp_plan* plans, uint32_t M, ltgp_record* out,
+                            int* size_limit_hit) {
+    if (!e || !plans || !size_limit_hit) { set_err("null argument"); return -1; }
+    TRY(ltgp_execute_generation_launch(e, plans, M));
+    return ltgp_execute_generation_finish(e, out, size_limit_hit);
 }
 
 int ltgp_subtree_extents(ltgp_engine* e, uint32_t count, const uint32_t* slots, const uint32_t* points,

@@ -152,7 +152,8 @@ __device__ __forceinline__ uint4 ld16_unaligned(const uint8_t* src) {
 __global__ void __launch_bounds__(256) k_splice(const PlanDev* plans, uint32_t count,
                                                 const DirEntry* dir, const Extent* ext,
                                                 const uint64_t* child_off, const uint64_t* child_size,
-                                                uint8_t* arena) {
+                                                uint8_t* arena, const uint32_t* skip) {
+    if (skip && *skip) return;  // device-resident generation: a limit or capacity check failed
     for (uint32_t c = blockIdx.x; c < count; c += gridDim.x) {
         const PlanDev p = plans[c];
         const Extent x = ext[c];

@@ -53,47 +53,94 @@ inline constexpr std::uint64_t splitmix64(std::uint64_t x) {
 // checkpoints read and write the same form; ltgp_host_rng_selftest checks
 // outputs and text against std::mt19937_64. plan_generation is bound by
 // this stream (64K draws per 4000-child generation).
+//
+// Blocks (one twist's state and its 312 tempered outputs) live in a ring:
+// prefill(n) twists ahead so the next n draws are loads, which the run loop
+// does while the device executes a generation (ltgp_execute_generation_launch
+// .. _finish). The stream is the same with or without prefill.
 class Mt64 {
 public:
     static constexpr int kN = 312, kM = 156;
-    explicit Mt64(std::uint64_t s) {
-        x_[0] = s;
-        for (int i = 1; i < kN; ++i) x_[i] = 6364136223846793005ull * (x_[i - 1] ^ (x_[i - 1] >> 62)) + (std::uint64_t)i;
+    explicit Mt64(std::uint64_t s) : ring_(4) {
+        std::uint64_t* x = ring_[0].x;
+        x[0] = s;
+        for (int i = 1; i < kN; ++i) x[i] = 6364136223846793005ull * (x[i - 1] ^ (x[i - 1] >> 62)) + (std::uint64_t)i;
+        temper(ring_[0]);
         p_ = kN;
     }
     std::uint64_t operator()() {
-        if (p_ >= kN) refill();
-        return out_[p_++];
+        if (p_ >= kN) advance();
+        return ring_[cur_].out[p_++];
+    }
+    // twist ahead until the next n draws need no twist
+    void prefill(std::uint64_t n) {
+        const std::uint64_t have = (std::uint64_t)(kN - p_) + (std::uint64_t)ahead_ * kN;
+        if (n <= have) return;
+        const std::size_t blocks = (std::size_t)((n - have + kN - 1) / kN);
+        if (ahead_ + blocks + 1 > ring_.size()) {  // grow, keeping current .. ahead in order
+            std::vector<Block> r(std::max(2 * ring_.size(), ahead_ + blocks + 1));
+            for (std::size_t i = 0; i <= ahead_; ++i) r[i] = ring_[(cur_ + i) % ring_.size()];
+            ring_.swap(r);
+            cur_ = 0;
+        }
+        for (std::size_t i = 0; i < blocks; ++i) {
+            const std::size_t src = (cur_ + ahead_) % ring_.size();
+            twist(ring_[src], ring_[(src + 1) % ring_.size()]);
+            ++ahead_;
+        }
     }
     friend std::ostream& operator<<(std::ostream& os, const Mt64& m) {
-        for (int i = 0; i < kN; ++i) os << m.x_[i] << ' ';
+        const std::uint64_t* x = m.ring_[m.cur_].x;
+        for (int i = 0; i < kN; ++i) os << x[i] << ' ';
         return os << m.p_;
     }
     friend std::istream& operator>>(std::istream& is, Mt64& m) {
-        for (int i = 0; i < kN; ++i) is >> m.x_[i];
-        is >> m.p_;
-        if (is && m.p_ > (unsigned)kN) is.setstate(std::ios::failbit);
-        if (is) m.temper_all();
+        Block b;
+        unsigned p = 0;
+        for (int i = 0; i < kN; ++i) is >> b.x[i];
+        is >> p;
+        if (is && p > (unsigned)kN) is.setstate(std::ios::failbit);
+        if (is) {
+            temper(b);
+            m.ring_.assign(4, Block{});
+            m.ring_[0] = b;
+            m.cur_ = 0;
+            m.ahead_ = 0;
+            m.p_ = p;
+        }
         return is;
     }
 
 private:
     friend class Rng;
-    // the twist and the tempering of all 312 outputs (ltgp_host.cpp: one
-    // clone per vector ISA, AVX2 / AVX-512 where the host has it)
-    void refill();
-    void temper_all() {
+    struct Block {
+        std::uint64_t x[kN];    // the state after this block's twist
+        std::uint64_t out[kN];  // its tempered outputs
+    };
+    // next block: prefilled, or twisted now
+    void advance() {
+        const std::size_t nx = (cur_ + 1) % ring_.size();
+        if (ahead_ == 0) twist(ring_[cur_], ring_[nx]);
+        else --ahead_;
+        cur_ = nx;
+        p_ = 0;
+    }
+    const std::uint64_t* out() const { return ring_[cur_].out; }
+    // dst = the twist of src, tempered (ltgp_host.cpp: one clone per vector
+    // ISA, AVX2 / AVX-512 where the host has it)
+    static void twist(const Block& src, Block& dst);
+    static void temper(Block& b) {
         for (int i = 0; i < kN; ++i) {
-            std::uint64_t z = x_[i];
+            std::uint64_t z = b.x[i];
             z ^= (z >> 29) & 0x5555555555555555ull;
             z ^= (z << 17) & 0x71d67fffeda60000ull;
             z ^= (z << 37) & 0xfff7eee000000000ull;
             z ^= z >> 43;
-            out_[i] = z;
+            b.out[i] = z;
         }
     }
-    std::uint64_t x_[kN];
-    std::uint64_t out_[kN];
+    std::vector<Block> ring_;
+    std::size_t cur_ = 0, ahead_ = 0;  // current block, blocks twisted beyond it
     unsigned p_;
 };
 
@@ -121,6 +168,8 @@ public:
         return static_cast<float>(2.0 * u - 1.0);
     }
     std::uint64_t draw_count() const { return draws_; }
+    // twist ahead so the next n draws are loads (same stream)
+    void prefill(std::uint64_t n) { engine_.prefill(n); }
 
     // The same stream for a hot loop (plan_generation's 64K draws per
     // generation): the stream position and the draw count live in the
@@ -130,7 +179,7 @@ public:
     // must not be used directly while a cursor on it is alive.
     class Cursor {
     public:
-        explicit Cursor(Rng& r) : r_(r), out_(r.engine_.out_), p_(r.engine_.p_) {}
+        explicit Cursor(Rng& r) : r_(r), out_(r.engine_.out()), p_(r.engine_.p_) {}
         ~Cursor() {
             r_.engine_.p_ = p_;
             r_.draws_ += draws_;
@@ -139,7 +188,8 @@ public:
         Cursor& operator=(const Cursor&) = delete;
         std::uint64_t raw() {
             if (p_ >= (unsigned)Mt64::kN) [[unlikely]] {
-                r_.engine_.refill();
+                r_.engine_.advance();
+                out_ = r_.engine_.out();
                 p_ = 0;
             }
             return out_[p_++];
@@ -158,7 +208,6 @@ public:
             }
             return static_cast<std::uint64_t>(m >> 64);
         }
-
     private:
         Rng& r_;
         const std::uint64_t* out_;

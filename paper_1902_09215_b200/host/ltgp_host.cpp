@@ -9,6 +9,7 @@
 #include "ltgp/ltgp.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -199,28 +200,31 @@ std::size_t tournament(Rng& rng, std::span<const Individual> pop, std::uint32_t 
 // Mt64's twist + tempering, vectorised per host ISA: the draws that bound
 // plan_generation cost 2.7 ns each with SSE2 and 1.2 ns with AVX2 on a Xeon
 // host (64K draws per 4000-child generation). Same outputs on every clone.
+// Out of place: dst.x[k] from src.x[k], src.x[k+1] and x[k+M] (src's for
+// k < N-M, already twisted dst's after).
 __attribute__((target_clones("avx512f", "avx2", "default")))
-void Mt64::refill() {
+void Mt64::twist(const Block& src, Block& dst) {
     constexpr std::uint64_t kUM = ~0ull << 31, kLM = ~kUM, kA = 0xb5026f5aa96619e9ull;
+    const std::uint64_t* x = src.x;
+    std::uint64_t* y = dst.x;
     for (int k = 0; k < kN - kM; ++k) {
-        const std::uint64_t y = (x_[k] & kUM) | (x_[k + 1] & kLM);
-        x_[k] = x_[k + kM] ^ (y >> 1) ^ ((0 - (y & 1)) & kA);
+        const std::uint64_t v = (x[k] & kUM) | (x[k + 1] & kLM);
+        y[k] = x[k + kM] ^ (v >> 1) ^ ((0 - (v & 1)) & kA);
     }
     for (int k = kN - kM; k < kN - 1; ++k) {
-        const std::uint64_t y = (x_[k] & kUM) | (x_[k + 1] & kLM);
-        x_[k] = x_[k + kM - kN] ^ (y >> 1) ^ ((0 - (y & 1)) & kA);
+        const std::uint64_t v = (x[k] & kUM) | (x[k + 1] & kLM);
+        y[k] = y[k + kM - kN] ^ (v >> 1) ^ ((0 - (v & 1)) & kA);
     }
-    const std::uint64_t y = (x_[kN - 1] & kUM) | (x_[0] & kLM);
-    x_[kN - 1] = x_[kM - 1] ^ (y >> 1) ^ ((0 - (y & 1)) & kA);
+    const std::uint64_t v = (x[kN - 1] & kUM) | (y[0] & kLM);
+    y[kN - 1] = y[kM - 1] ^ (v >> 1) ^ ((0 - (v & 1)) & kA);
     for (int i = 0; i < kN; ++i) {
-        std::uint64_t z = x_[i];
+        std::uint64_t z = y[i];
         z ^= (z >> 29) & 0x5555555555555555ull;
         z ^= (z << 17) & 0x71d67fffeda60000ull;
         z ^= (z << 37) & 0xfff7eee000000000ull;
         z ^= z >> 43;
-        out_[i] = z;
+        dst.out[i] = z;
     }
-    p_ = 0;
 }
 
 // evolve.hpp:84-87. The tournaments read fitness from a
@@ -241,8 +245,10 @@ static inline std::uint32_t selection_key(float f) {
 // tournament (evolve.hpp:79-82) on selection keys: the same draws and the
 // same winner as tournament_by(fitness_better, fitness_tied). The running
 // best is one packed (key << 32 | index) word, so "better" is an unsigned
-// min (a cmov: the data-dependent branch it replaces mispredicted on ~1.6
-// of every 6 entrants); only a tie, which draws, branches.
+// min (a cmov). A tie keeps its branch: its draw moves the stream position,
+// and a branch-free conditional increment puts every later draw's load
+// behind the comparison chain (measured 1.3-3x slower than predicting, even
+// on evolved populations where ~3 of 4 entrants tie).
 static inline std::size_t tournament_keys(Rng::Cursor& rng, std::uint64_t M, std::uint32_t k, const std::uint32_t* key) {
     const std::uint64_t b0 = rng.below(M);
     std::uint64_t pb = (std::uint64_t)key[b0] << 32 | b0;
@@ -307,16 +313,22 @@ void evaluate_population(std::vector<Individual>& population, ExecContext ctx) {
 
 // evolve.hpp:111-117 on the engine. `parents` must be the engine's current
 // population (from evaluate_population or a previous execute_generation).
-ExecOutcome execute_generation(std::span<const CrossoverPlan> plans, std::vector<Individual>& parents,
-                               std::vector<Individual>& children, ExecContext ctx) {
+// execute_generation in two halves (ltgp_execute_generation_launch /
+// _finish): the run loop twists the next generation's Rng blocks in between.
+static void execute_generation_begin(std::span<const CrossoverPlan> plans, const std::vector<Individual>& parents,
+                                     const ExecContext& ctx) {
     if (!ctx.engine) throw std::invalid_argument("ExecContext.engine is null");
     if (plans.size() != parents.size()) throw std::invalid_argument("one plan per child slot");
-    std::vector<ltgp_record> rec(plans.size());
-    int hit = 0;
     check(ltgp_set_memory_budget(ctx.engine, ctx.config.memory_budget_bytes));
     if (ctx.config.streaming_memory) check(ltgp_set_streaming(ctx.engine, 1, 0));  // evolve.hpp:45
-    check(ltgp_execute_generation(ctx.engine, plans.data(), static_cast<std::uint32_t>(plans.size()),
-                                  rec.data(), &hit));
+    check(ltgp_execute_generation_launch(ctx.engine, plans.data(), static_cast<std::uint32_t>(plans.size())));
+}
+
+static ExecOutcome execute_generation_end(std::span<const CrossoverPlan> plans, std::vector<Individual>& parents,
+                                          std::vector<Individual>& children, ExecContext ctx) {
+    std::vector<ltgp_record> rec(plans.size());
+    int hit = 0;
+    check(ltgp_execute_generation_finish(ctx.engine, rec.data(), &hit));
     if (hit == 2) return ExecOutcome{false, true};  // MemoryBudgetExceeded: nothing was built
     if (hit) return ExecOutcome{true, false};
     children.resize(plans.size());
@@ -327,6 +339,12 @@ ExecOutcome execute_generation(std::span<const CrossoverPlan> plans, std::vector
     ctx.gauge.add(static_cast<std::int64_t>(plans.size()));
     ctx.gauge.sub(static_cast<std::int64_t>(parents.size()));
     return ExecOutcome{false, false};
+}
+
+ExecOutcome execute_generation(std::span<const CrossoverPlan> plans, std::vector<Individual>& parents,
+                               std::vector<Individual>& children, ExecContext ctx) {
+    execute_generation_begin(plans, parents, ctx);
+    return execute_generation_end(plans, parents, children, ctx);
 }
 
 namespace {
@@ -447,6 +465,16 @@ int ltgp_host_rng_selftest(void) {
         for (int i = 0; i < 2000; ++i) {
             const uint64_t x = a(), y = b(), z = c(), w = d();
             if (x != y || x != z || x != w) return 3;
+        }
+        // prefill (ring growth included) leaves the stream and its text unchanged
+        for (const uint64_t n : {1ull, 311ull, 5000ull, 100000ull}) {
+            a.prefill(n);
+            for (uint64_t i = 0; i < n / 2 + 7; ++i)
+                if (a() != b()) return 4;
+            std::ostringstream ta, tb;
+            ta << a;
+            tb << b;
+            if (ta.str() != tb.str()) return 5;
         }
     }
     return 0;
@@ -804,9 +832,27 @@ int64_t ltgp_host_run_checkpointed(ltgp_engine* e, uint32_t M, uint32_t G, uint6
             if (ckpt_every) checkpoint(0);
         }
         int64_t done = gen0;
+        // LTGP_TRACE=1: host wall time of each generation's planning and
+        // execution (the engine adds its own phase marks)
+        static const bool trace = std::getenv("LTGP_TRACE") != nullptr;
+        uint64_t draws = 0;  // the last generation's Rng draws
         for (uint32_t gen = gen0 + 1; gen <= G; ++gen) {
+            const auto t0 = std::chrono::steady_clock::now();
+            const uint64_t d0 = rng.draw_count();
             const auto plans = plan_generation(rng, pop, k);
-            const ExecOutcome o = execute_generation(plans, pop, next, ctx);
+            draws = rng.draw_count() - d0;
+            const auto t1 = std::chrono::steady_clock::now();
+            execute_generation_begin(plans, pop, ctx);
+            // while the device runs the generation: the next one's Rng blocks
+            // (its draws are a tie or two away from this one's)
+            rng.prefill(draws + draws / 8 + 1024);
+            const ExecOutcome o = execute_generation_end(plans, pop, next, ctx);
+            if (trace) {
+                const auto t2 = std::chrono::steady_clock::now();
+                std::fprintf(stderr, "[ltgp] gen %u: plan_generation %.1f us, execute_generation %.1f us, %llu draws\n",
+                             gen, std::chrono::duration<double, std::micro>(t1 - t0).count(),
+                             std::chrono::duration<double, std::micro>(t2 - t1).count(), (unsigned long long)draws);
+            }
             if (o.memory_budget_exceeded) { *reason = 2; break; }  // TerminationReason (evolve.hpp:34)
             if (o.size_limit_hit) { *reason = 1; break; }
             std::swap(pop, next);
