@@ -74,6 +74,8 @@ typedef struct {
     uint64_t live_genomes_high_water; /* streaming memory mode: most live genomes (parents not yet
                                          retired + children built) seen at a wave boundary */
     uint64_t arena_used_high_water;   /* streaming memory mode: most arena bytes holding live genomes */
+    uint64_t last_h2d_bytes;    /* host-to-device bytes of the last ltgp_evaluate_packed (packed slices,
+                                   ltgp_pack.h; the raw bytes with LTGP_PACK=0) */
 } ltgp_stats;
 
 /* Generation statistics of the current population (GenerationStats,
@@ -130,8 +132,10 @@ int ltgp_evaluate_outputs(ltgp_engine* e, ltgp_record* out, float* outs48);
    the packed buffer (same layout rules as ltgp_upload_packed) becomes the
    population and is evaluated while it uploads. Slices of ~16 MB go
    host-to-device on a copy stream and each slice's trees are evaluated as
-   soon as they land. buf should be pinned (pageable memory works but
-   serialises the copy). out: M records; outs48: per-case outputs or NULL. */
+   soon as they land. Each slice is packed on the host first (ltgp_pack_host:
+   ~0.63 B per node instead of 1, host threads; LTGP_PACK=0 sends the raw
+   bytes) and rebuilt into the arena on the device. out: M records;
+   outs48: per-case outputs or NULL. */
 int ltgp_evaluate_packed(ltgp_engine* e, uint32_t M, const uint8_t* buf, uint64_t buf_bytes,
                          const uint64_t* offsets, const uint64_t* sizes, ltgp_record* out,
                          float* outs48);
@@ -206,6 +210,14 @@ uint32_t ltgp_population_size(ltgp_engine* e);
    callers that run their own collective (e.g. torch.distributed NCCL). */
 int ltgp_shard_records(ltgp_engine* e, int s, void** dev_records, uint32_t* first,
                        uint32_t* count, void** stream);
+
+/* The packed form a streamed evaluation sends over PCIe (ltgp_pack.h:
+   3-bit codes for opcodes 0-4 and 0xFF, literal bytes for the rest), exposed
+   for tests and tools. ltgp_pack_bound: the buffer size packing `len` bytes
+   may need. ltgp_pack_host packs src[0, len) into dst with `threads` host
+   threads and returns the packed size (0 on error). */
+uint64_t ltgp_pack_bound(uint64_t len);
+uint64_t ltgp_pack_host(const uint8_t* src, uint64_t len, uint8_t* dst, int threads);
 
 #ifdef __cplusplus
 }

@@ -57,7 +57,8 @@ class _Stats(C.Structure):
                 ("last_fallback_items", C.c_uint64), ("last_exits", C.c_uint64),
                 ("last_window_adjusts", C.c_uint64), ("last_spine_steps", C.c_uint64),
                 ("kernel_launches", C.c_uint32), ("gather_nccl", C.c_uint32), ("keval_seconds", C.c_double),
-                ("live_genomes_high_water", C.c_uint64), ("arena_used_high_water", C.c_uint64)]
+                ("live_genomes_high_water", C.c_uint64), ("arena_used_high_water", C.c_uint64),
+                ("last_h2d_bytes", C.c_uint64)]
 
 
 _cuda = None
@@ -93,6 +94,8 @@ _CUDA_SIGS = {
     "ltgp_population_size": (C.c_uint32, [_P]),
     "ltgp_shard_records": (C.c_int, [_P, C.c_int, C.POINTER(_P), C.POINTER(C.c_uint32),
                                      C.POINTER(C.c_uint32), C.POINTER(_P)]),
+    "ltgp_pack_bound": (C.c_uint64, [C.c_uint64]),
+    "ltgp_pack_host": (C.c_uint64, [_P, C.c_uint64, _P, C.c_int]),
 }
 _HOST_SIGS = {
     "ltgp_host_splitmix64": (C.c_uint64, [C.c_uint64]),
@@ -161,6 +164,18 @@ def _err():
 def _check(status):
     if status != 0:
         raise EngineError(_err())
+
+
+def pack_host(buf: np.ndarray, threads: int = 1) -> np.ndarray:
+    """The packed PCIe form of a byte range (ltgp_pack.h), as a streamed
+    evaluation sends it: host code, no GPU needed."""
+    buf = np.ascontiguousarray(buf, dtype=np.uint8)
+    lib = cuda_lib()
+    out = np.zeros(lib.ltgp_pack_bound(buf.nbytes), dtype=np.uint8)
+    n = lib.ltgp_pack_host(_ptr(buf), buf.nbytes, _ptr(out), threads)
+    if n == 0 and buf.nbytes:
+        raise EngineError(_err())
+    return out[:n]
 
 
 # --------------------------------------------------------------------------

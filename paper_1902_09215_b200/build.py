@@ -19,6 +19,9 @@ CSRC = os.path.join(PKG, "csrc")
 HOST = os.path.join(PKG, "host")
 
 CUDA_LIB = os.path.join(PKG, "libltgp_cuda.so")
+# host packing of streamed slices (csrc/ltgp_pack.h): g++, linked into CUDA_LIB
+PACK_SRC = os.path.join(CSRC, "ltgp_pack.cpp")
+PACK_OBJ = os.path.join(CSRC, "ltgp_pack.o")
 HOST_LIB = os.path.join(PKG, "libltgp_host.so")
 
 # Bit-exactness flags: one IEEE RN op per node, no
@@ -62,9 +65,11 @@ def _deps(dirname, exts):
 
 def build(force: bool = False, verbose: bool = False) -> None:
     nvcc = os.environ.get("NVCC", "nvcc")
-    cu_deps = _deps(CSRC, (".cu", ".cuh")) + [os.path.join(ROOT, "include", "ltgp_cuda.h")]
+    cu_deps = _deps(CSRC, (".cu", ".cuh", ".h")) + [os.path.join(ROOT, "include", "ltgp_cuda.h")]
+    cu_deps += [PACK_SRC]
     if force or _stale(CUDA_LIB, cu_deps):
-        _run([nvcc, *NVCC_FLAGS, "-shared", "-o", CUDA_LIB, os.path.join(CSRC, "ltgp_engine.cu")],
+        _run(["g++", *CXX_FLAGS, "-c", "-o", PACK_OBJ, PACK_SRC])
+        _run([nvcc, *NVCC_FLAGS, "-shared", "-o", CUDA_LIB, os.path.join(CSRC, "ltgp_engine.cu"), PACK_OBJ],
              log=os.path.join(CSRC, "ptxas.log"))
     host_deps = _deps(HOST, (".cpp", ".hpp")) + [os.path.join(ROOT, "include", "ltgp_host.h"), CUDA_LIB]
     if force or _stale(HOST_LIB, host_deps):

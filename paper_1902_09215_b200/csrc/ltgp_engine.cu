@@ -22,11 +22,13 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/ltgp_cuda.h"
 #include "ltgp_gen.cuh"
 #include "ltgp_kernels.cuh"
+#include "ltgp_pack.h"
 #include "ltgp_splice.cuh"
 
 using namespace ltgp_dev;
@@ -184,6 +186,7 @@ uint64_t g_version = 0;
 struct Slice {
     uint32_t tree_begin;
     uint64_t src, dst, len;
+    uint64_t pk_off = 0;  // packed transfer (ltgp_pack.h): the slice's region in the staging buffers
 };
 constexpr uint32_t kMaxSlices = 64;
 constexpr int kComputeStreams = 4;     // slice g runs on compute stream g % 4
@@ -204,12 +207,49 @@ uint64_t slice_bytes() {
 }
 uint32_t max_slices() {
     const char* v = std::getenv("LTGP_SLICES");
-    return v ? (uint32_t)std::min<long>(kMaxSlices, std::max<long>(1, std::strtol(v, nullptr, 10))) : 24u;
+    // 48: the cross-slice launch takes each slice as it lands, so finer
+    // slices start the device sooner (config 3: 16.2 ms at 48, 16.9 at 24)
+    return v ? (uint32_t)std::min<long>(kMaxSlices, std::max<long>(1, std::strtol(v, nullptr, 10))) : 48u;
+}
+// packed PCIe transfer of streamed evaluations (LTGP_PACK=0 sends raw bytes)
+// and its host threads (LTGP_PACK_THREADS, default: every hardware thread but one)
+bool pack_enabled() {
+    const char* v = std::getenv("LTGP_PACK");
+    return !v || std::atoi(v) != 0;
+}
+int pack_threads() {  // the calling thread launches the slices' kernels meanwhile: one core for it
+    const char* v = std::getenv("LTGP_PACK_THREADS");
+    const int n = v ? std::atoi(v) : (int)std::thread::hardware_concurrency() - 1;
+    return std::max(1, std::min(n, 256));
 }
 constexpr uint32_t kQueueBase = 16;    // counters[16 + g]: work queue of slice g
 constexpr uint32_t kPoolCounters = 8;  // counters[8..11]: chunk-summary pool claims (2 x u64)
-constexpr size_t kCounterBytes = 512;
-static_assert(kCounterBytes >= 4 * (kQueueBase + kMaxSlices), "every slice needs its queue counter");
+constexpr uint32_t kXFlagBase = kQueueBase + kMaxSlices;  // counters[kXFlagBase ..): cross-slice flags (3 per slice)
+constexpr size_t kCounterBytes = 2048;
+static_assert(kCounterBytes >= 4 * (kXFlagBase + 3 * kMaxSlices), "every slice needs its queue counter and flags");
+static_assert(kMaxSlices == kMaxXSlices, "one flag triple per slice");
+// A packed streamed evaluation runs ONE persistent k_eval that also decodes
+// and plans each slice as its bytes land (per-slice launches each left a
+// drained-CTA tail and waited for SMs to plan): LTGP_XSLICE=0 selects the
+// per-slice launches
+bool xslice_enabled() {
+    const char* v = std::getenv("LTGP_XSLICE");
+    return !v || std::atoi(v) != 0;
+}
+// cuStreamWriteValue32 (driver API, found at run time): the copy stream marks
+// a slice copied without a kernel (every SM may be busy in k_eval)
+typedef int (*StreamWriteValue32)(cudaStream_t, unsigned long long, uint32_t, unsigned int);
+StreamWriteValue32 stream_write_value32() {
+    static StreamWriteValue32 f = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<StreamWriteValue32>(fn);
+    }();
+    return f;
+}
 
 struct Shard {
     int dev = 0;
@@ -219,6 +259,11 @@ struct Shard {
     std::vector<cudaEvent_t> sev;               // 3 per slice: copied, planned, evaluated
     std::vector<Slice> slices;                  // non-empty during a streamed evaluation
     const uint8_t* src = nullptr;               // its pinned host source
+    HostBuf pk_host;                            // packed slices (ltgp_pack.h), pinned, one region per slice
+    DevBuf pk_dev;                              // and their device copies
+    uint64_t h2d_bytes = 0;                     // bytes the last streamed evaluation sent
+    HostBuf h_xsl;                              // cross-slice launch: the slice descriptors (XSlice)
+    DevBuf xsl;
     std::vector<uint32_t> slice_items;          // slice g's items: [slice_items[g], slice_items[g+1])
     std::vector<uint32_t> slice_ct, slice_ch;   // slice g's chunked trees / chunks (same convention)
     std::vector<uint32_t> items_slices;         // work-list cache key (slice tree boundaries)
@@ -281,6 +326,7 @@ struct Shard {
         h_items.release(); h_ctrees.release(); h_counters.release();
         h_csize.release(); h_coff.release(); h_dir.release();
         for (auto& b : xspill) b.release();
+        pk_host.release(); pk_dev.release(); h_xsl.release(); xsl.release();
         if (st) { cudaSetDevice(dev); cudaStreamDestroy(st); }
         for (int k = 1; k < kComputeStreams; ++k) if (xs[k]) cudaStreamDestroy(xs[k]);
         if (cst) cudaStreamDestroy(cst);
@@ -311,6 +357,7 @@ struct ltgp_engine {
     uint64_t used_high_water = 0;    // arena bytes holding live genomes
     ltgp_stats stats;
     HostBuf staging;
+    ltgp_pack::Pool* pack = nullptr;  // host packing threads of streamed evaluations (ltgp_pack.h)
     // ltgp_execute_generation_launch .. _finish
     struct Pending {
         bool active = false, device = false;
@@ -353,7 +400,9 @@ uint32_t spill_frames(uint32_t C) {
     while (f < want) f *= 2;
     return f;
 }
-#define K_EVAL k_eval<kWarps, kWindow>
+#define K_EVAL k_eval<kWarps, kWindow, false>
+#define K_EVAL_XS k_eval<kWarps, kWindow, true>
+static_assert(kWindow == kPlanWindow, "the plan tasks use the interpreter's window");
 
 int init_shard(ltgp_engine* e, Shard& s) {
     CK(cudaSetDevice(s.dev));
@@ -375,6 +424,7 @@ int init_shard(ltgp_engine* e, Shard& s) {
     s.sms = prop.multiProcessorCount;
     const size_t smem = eval_smem_bytes();
     CK(cudaFuncSetAttribute(K_EVAL, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(K_EVAL_XS, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CK(cudaFuncSetAttribute(k_cpops, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCpopsSmem));
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K_EVAL, kWarps * 32, smem));
@@ -633,6 +683,12 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     a.counters = s.counters.as<uint32_t>();
     a.queue = s.counters.as<uint32_t>();
     a.item_base = 0;
+    a.xsl = nullptr;
+    a.n_xs = 0;
+    a.n_tasks = 0;
+    a.xflags = nullptr;
+    a.meta = nullptr;
+    a.xs_skip = 0;
     a.hdr = s.hdr.as<ChunkHdr>();
     a.steps = s.steps.as<uint8_t>();
     a.frames = s.frames.as<float2>();
@@ -679,6 +735,44 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     CK(cudaEventRecord(s.ev[0], s.st));
     s.kev_valid = false;
     uint32_t launches = 0;
+    const bool xslice = streamed && G > 1 && nitems && e->pack && xslice_enabled() && stream_write_value32();
+    if (xslice) {
+        // one k_eval for every slice on s.st: its warps decode, plan and
+        // evaluate each slice once the copy stream has marked it copied
+        TRY(s.h_xsl.ensure(sizeof(XSlice) * G));
+        TRY(s.xsl.ensure(sizeof(XSlice) * G, s.dev));
+        XSlice* hx = s.h_xsl.as<XSlice>();
+        uint32_t task = 0;
+        for (uint32_t g = 0; g < G; ++g) {
+            const Slice& sl = s.slices[g];
+            const ltgp_pack::Layout L(sl.len);
+            XSlice& x = hx[g];
+            x.pk = s.pk_dev.as<uint8_t>() + sl.pk_off;
+            x.plane_bytes = L.plane_bytes;
+            x.base_off = L.base_off;
+            x.lit_off = L.lit_off;
+            x.npk = L.npk;
+            x.p_lo = sl.dst / 16;
+            x.task0 = task;
+            x.nd = (uint32_t)L.nblk;
+            x.np = s.slice_items[g + 1] - s.slice_items[g];
+            x.item0 = s.slice_items[g];
+            task += x.nd + 2 * x.np;
+        }
+        CK(cudaMemcpyAsync(s.xsl.p, hx, sizeof(XSlice) * G, cudaMemcpyHostToDevice, s.st));
+        EvalArgs ag = a;
+        ag.xsl = s.xsl.as<XSlice>();
+        ag.n_xs = G;
+        ag.n_tasks = task;
+        ag.xflags = s.counters.as<uint32_t>() + kXFlagBase;
+        ag.meta = ts.meta.as<uint32_t>();
+        ag.pool = pool;
+        ag.queue = s.counters.as<uint32_t>() + kQueueBase;
+        ag.xs_skip = std::getenv("LTGP_XS_SKIP") ? (uint32_t)std::atoi(std::getenv("LTGP_XS_SKIP")) : 0u;
+        K_EVAL_XS<<<s.eval_grid, kWarps * 32, eval_smem_bytes(), s.st>>>(ag, e->suite);
+        CK(cudaGetLastError());
+        ++launches;
+    }
     for (uint32_t g = 0; g < G; ++g) {
         const uint32_t xk = g % kComputeStreams;
         cudaStream_t X = s.xs[xk];
@@ -686,9 +780,38 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         if (streamed) {
             const Slice& sl = s.slices[g];
             if (g == 0) CK(cudaStreamWaitEvent(s.cst, s.ev[0], 0));  // counters cleared, arena free
-            CK(cudaMemcpyAsync(ts.arena.as<uint8_t>() + sl.dst, s.src + sl.src, sl.len, cudaMemcpyHostToDevice,
-                               s.cst));
+            if (e->pack) {
+                // packed transfer: the host threads pack this slice (~0.63 B per
+                // node instead of 1) while the previous slices are in flight;
+                // the next slice's packing starts before this one's kernels
+                // are launched
+                NvtxRange nr_pack("ltgp.pack");
+                // (the cross-slice launch leaves the calling thread idle: it packs too)
+                if (g == 0)
+                    ltgp_pack::pack_start(e->pack, s.src + sl.src, sl.len, s.pk_host.as<uint8_t>() + sl.pk_off, xslice);
+                const uint64_t nb = ltgp_pack::pack_wait(e->pack);
+                CK(cudaMemcpyAsync(s.pk_dev.as<uint8_t>() + sl.pk_off, s.pk_host.as<uint8_t>() + sl.pk_off, nb,
+                                   cudaMemcpyHostToDevice, s.cst));
+                if (g + 1 < G) {
+                    const Slice& nx = s.slices[g + 1];
+                    ltgp_pack::pack_start(e->pack, s.src + nx.src, nx.len, s.pk_host.as<uint8_t>() + nx.pk_off, xslice);
+                }
+                s.h2d_bytes += nb;
+            } else {
+                CK(cudaMemcpyAsync(ts.arena.as<uint8_t>() + sl.dst, s.src + sl.src, sl.len, cudaMemcpyHostToDevice,
+                                   s.cst));
+                s.h2d_bytes += sl.len;
+            }
             CK(cudaEventRecord(s.sev[3 * g], s.cst));
+            if (xslice) {  // the slice's decode tasks may start
+                const unsigned long long flag =
+                    reinterpret_cast<unsigned long long>(s.counters.as<uint32_t>() + kXFlagBase + g);
+                if (stream_write_value32()(s.cst, flag, 1u, 0u) != 0) {
+                    set_err("cuStreamWriteValue32 failed");
+                    return -1;
+                }
+                continue;
+            }
             CK(cudaStreamWaitEvent(X, s.sev[3 * g], 0));
             // the previous slice's records are final before this slice's
             // kernels (its k_eval's look-ahead may read them)
@@ -710,7 +833,17 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         const bool plan_warp = plan_mode != 0;
         const bool fuse_decode = plan_warp && !streamed;
         NvtxRange nr_plan("ltgp.decode+plan");
-        if (p_hi > p_lo && !fuse_decode) {
+        if (p_hi > p_lo && streamed && e->pack) {  // rebuild the slice's bytes into the arena, decoding them
+            const Slice& sl = s.slices[g];
+            const ltgp_pack::Layout L(sl.len);
+            const uint64_t blocks = std::min<uint64_t>(L.nblk, (uint64_t)s.sms * 8);
+            k_decode_packed<<<(unsigned)blocks, kPackBlock, 0, X>>>(
+                s.pk_dev.as<uint8_t>() + sl.pk_off, L.plane_bytes, L.base_off, L.lit_off, L.npk, ts.arena.as<uint4>(),
+                dec, ts.meta.as<uint32_t>(), packets, p_lo);
+            CK(cudaGetLastError());
+            DEBUG_SYNC(X, "k_decode_packed");
+            ++launches;
+        } else if (p_hi > p_lo && !fuse_decode) {
             const uint64_t blocks = std::min<uint64_t>((p_hi - p_lo + 255) / 256, (uint64_t)s.sms * 16);
             k_decode<<<(unsigned)blocks, 256, 0, X>>>(ts.arena.as<uint4>(), dec, ts.meta.as<uint32_t>(), packets,
                                                      p_lo, p_hi);
@@ -770,11 +903,17 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         }
         if (streamed) CK(cudaEventRecord(s.sev[3 * g + 2], X));
     }
-    if (streamed)  // join the other compute streams: the last slice each ran
+    if (xslice) {  // k_eval has waited for every copy; the trace's plan / eval marks are its end
+        for (uint32_t g = 0; g < G; ++g) {
+            CK(cudaEventRecord(s.sev[3 * g + 1], s.st));
+            CK(cudaEventRecord(s.sev[3 * g + 2], s.st));
+        }
+    } else if (streamed) {  // join the other compute streams: the last slice each ran
         for (uint32_t g = G > (uint32_t)kComputeStreams ? G - kComputeStreams : 0; g < G; ++g)
             if (g % kComputeStreams) CK(cudaStreamWaitEvent(s.st, s.sev[3 * g + 2], 0));
+    }
     CK(cudaEventRecord(s.ev[4], s.st));
-    if (nct && !streamed) TRY(launch_combine(e, s, ca, s.st, launches));
+    if (nct && (!streamed || xslice)) TRY(launch_combine(e, s, ca, s.st, launches));
     CK(cudaEventRecord(s.ev[1], s.st));
     CK(cudaMemcpyAsync(s.h_counters.p, s.counters.p, 64, cudaMemcpyDeviceToHost, s.st));
     e->stats.kernel_launches = launches;
@@ -1230,6 +1369,8 @@ int ltgp_engine_destroy(ltgp_engine* e) {
     }
     release_gather(e);
     e->staging.release();
+    if (e->pack) ltgp_pack::pool_destroy(e->pack);
+    e->pack = nullptr;
     delete e;
     return 0;
 }
@@ -1437,7 +1578,12 @@ int ltgp_evaluate_packed(ltgp_engine* e, uint32_t M, const uint8_t* buf, uint64_
         s.slices.clear();
         // the last three slices taper (1/2, 1/4, 1/8 of the others): what is
         // left to evaluate after the final copy is short
-        auto weight = [&](uint32_t g) -> uint64_t { return G >= 4 && g + 3 >= G ? 8u >> (g + 4 - G) : 8u; };
+        // and so do the first two (1/4, 1/2): the evaluation starts after
+        // the first slice is packed and copied
+        auto weight = [&](uint32_t g) -> uint64_t {
+            if (G >= 8 && g < 2) return 2u << g;
+            return G >= 4 && g + 3 >= G ? 8u >> (g + 4 - G) : 8u;
+        };
         uint64_t wsum = 0;
         for (uint32_t g = 0; g < G; ++g) wsum += weight(g);
         uint64_t wcum = 0;
@@ -1457,6 +1603,17 @@ int ltgp_evaluate_packed(ltgp_engine* e, uint32_t M, const uint8_t* buf, uint64_
         const Slice& ls = s.slices.back();
         ts.bytes = ls.dst + ls.len;
         TRY(ts.arena.ensure(ts.bytes + 64, s.dev));
+        s.h2d_bytes = 0;
+        if (pack_enabled()) {  // packed transfer: worst-case regions per slice
+            if (!e->pack) e->pack = ltgp_pack::pool_create(pack_threads());
+            uint64_t o = 0;
+            for (Slice& sl : s.slices) {
+                sl.pk_off = o;  // 64-B aligned: the packer's non-temporal stores
+                o += ltgp_pack::ceil64(ltgp_pack::Layout(sl.len).max_bytes());
+            }
+            TRY(s.pk_host.ensure(o));
+            TRY(s.pk_dev.ensure(o, s.dev));
+        }
         TRY(upload_tables(s, ts));
         s.src = buf;
         const int rc = launch_eval(e, s, ts, outs48 != nullptr);
@@ -1478,7 +1635,19 @@ int ltgp_evaluate_packed(ltgp_engine* e, uint32_t M, const uint8_t* buf, uint64_
         TRY(rc);
     }
     e->M = M;
+    e->stats.last_h2d_bytes = 0;
+    for (const Shard& s : e->shards) e->stats.last_h2d_bytes += s.h2d_bytes;
     return collect(e, out, outs48);
+}
+
+uint64_t ltgp_pack_bound(uint64_t len) { return ltgp_pack::Layout(len).max_bytes(); }
+
+uint64_t ltgp_pack_host(const uint8_t* src, uint64_t len, uint8_t* dst, int threads) {
+    if ((!src && len) || !dst) { set_err("null argument"); return 0; }
+    ltgp_pack::Pool* P = ltgp_pack::pool_create(std::max(1, threads));
+    const uint64_t n = ltgp_pack::pack(P, src, len, dst);
+    ltgp_pack::pool_destroy(P);
+    return n;
 }
 
 int ltgp_evaluate_outputs(ltgp_engine* e, ltgp_record* out, float* outs48) {

@@ -441,6 +441,52 @@ def test_streamed_evaluate_packed_matches_resident(oracle, suite):
     assert_records_equal(got[idx], ref)
 
 
+def test_streamed_packed_transfer(oracle, suite, monkeypatch):
+    """The streamed path's packed PCIe form (ltgp_pack.h, k_decode_packed):
+    records, per-case outputs and the rebuilt arena equal the raw-byte
+    transfer (LTGP_PACK=0) and the oracle, with garbage (any byte value) in
+    the gaps between trees, constants of every opcode 5..254, slices of every
+    size down to one packet, and the scalar host encoder; the bytes sent are
+    ~0.63 per node on a config-3 corpus."""
+    rng = np.random.default_rng(5)
+    genomes = [ltgp.remy_tree(900 + k, n) for k, n in enumerate((1, 3, 15, 17, 33, 255, 4097, 30001, 123457))]
+    for g in genomes:  # every constant opcode
+        leaves = g >= X
+        g[leaves] = np.where(rng.random(leaves.sum()) < 0.3, X, rng.integers(5, 255, leaves.sum()))
+    buf, offs, sizes = pack(genomes)
+    for k in range(len(genomes)):  # garbage between trees: the arena keeps every byte
+        end = int(offs[k]) + int(sizes[k])
+        nxt = int(offs[k + 1]) if k + 1 < len(genomes) else buf.size
+        buf[end:nxt] = rng.integers(0, 256, nxt - end)
+    exp = oracle.evaluate_population(buf, offs, sizes, suite, threads=0)
+    results = []
+    for env in ({"LTGP_PACK": "0"}, {}, {"LTGP_SLICES": "64", "LTGP_SLICE_KB": "1"}, {"LTGP_PACK_THREADS": "3"}):
+        for k in ("LTGP_PACK", "LTGP_SLICES", "LTGP_SLICE_KB", "LTGP_PACK_THREADS"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        with engine(suite, chunk=1024) as e:
+            rec, outs = e.evaluate_packed(buf, offs, sizes, outputs=True)
+            arena = [e.download_genome(k) for k in range(len(genomes))]
+            h2d = e.stats()["last_h2d_bytes"]
+        assert_records_equal(rec, exp)
+        for k, g in enumerate(genomes):
+            assert np.array_equal(arena[k], g)
+            o, _ = oracle.eval_batch(g, suite[0], suite[2])
+            assert same_bits(outs[k], o)
+        results.append((rec.tobytes(), outs.tobytes(), h2d))
+    assert len({r[:2] for r in results}) == 1
+    assert results[0][2] <= buf.size and results[1][2] < results[0][2]
+    # config-3 corpus: ~0.63 bytes a node cross PCIe, records unchanged
+    monkeypatch.delenv("LTGP_PACK_THREADS")
+    cb, co, cs = ltgp.corpus(1, 400, 4.0, 5.0)
+    with engine(suite) as e:
+        e.upload_packed(cb, co, cs)
+        ref = e.evaluate_population()
+        assert e.evaluate_packed(cb, co, cs).tobytes() == ref.tobytes()
+        assert e.stats()["last_h2d_bytes"] < 0.66 * cb.size
+
+
 def test_streamed_small_and_outputs(oracle, suite):
     """A small population (one slice) with per-case outputs, from pageable memory."""
     genomes = [ltgp.remy_tree(70 + k, n) for k, n in enumerate((1, 3, 17, 1001, 20001, 70001))]

@@ -13,6 +13,7 @@ name = sys.argv[1]
 extra = sys.argv[2:]
 out = os.path.join(ROOT, "exp", name)
 os.makedirs(out, exist_ok=True)
+B._run(["g++", *B.CXX_FLAGS, "-c", "-o", os.path.join(out, "ltgp_pack.o"), B.PACK_SRC])
 B._run(["nvcc", *B.NVCC_FLAGS, *extra, "-shared", "-o", os.path.join(out, "libltgp_cuda.so"),
-        os.path.join(B.CSRC, "ltgp_engine.cu")], log=os.path.join(out, "ptxas.log"))
+        os.path.join(B.CSRC, "ltgp_engine.cu"), os.path.join(out, "ltgp_pack.o")], log=os.path.join(out, "ptxas.log"))
 print("built", out)
