@@ -226,7 +226,7 @@ constexpr uint32_t kQueueBase = 16;    // counters[16 + g]: work queue of slice 
 constexpr uint32_t kPoolCounters = 8;  // counters[8..11]: chunk-summary pool claims (2 x u64)
 constexpr uint32_t kXFlagBase = kQueueBase + kMaxSlices;  // counters[kXFlagBase ..): cross-slice flags (3 per slice)
 constexpr size_t kCounterBytes = 2048;
-static_assert(kCounterBytes >= 4 * (kXFlagBase + 3 * kMaxSlices), "every slice needs its queue counter and flags");
+static_assert(kCounterBytes >= 4 * (kXFlagBase + 4 * kMaxSlices), "every slice needs its queue counter and flags");
 static_assert(kMaxSlices == kMaxXSlices, "one flag triple per slice");
 // A packed streamed evaluation runs ONE persistent k_eval that also decodes
 // and plans each slice as its bytes land (per-slice launches each left a
@@ -263,7 +263,7 @@ struct Shard {
     DevBuf pk_dev;                              // and their device copies
     uint64_t h2d_bytes = 0;                     // bytes the last streamed evaluation sent
     HostBuf h_xsl;                              // cross-slice launch: the slice descriptors (XSlice)
-    DevBuf xsl;
+    DevBuf xsl, xtime;                          // and its trace timestamps (LTGP_TRACE)
     std::vector<uint32_t> slice_items;          // slice g's items: [slice_items[g], slice_items[g+1])
     std::vector<uint32_t> slice_ct, slice_ch;   // slice g's chunked trees / chunks (same convention)
     std::vector<uint32_t> items_slices;         // work-list cache key (slice tree boundaries)
@@ -326,7 +326,7 @@ struct Shard {
         h_items.release(); h_ctrees.release(); h_counters.release();
         h_csize.release(); h_coff.release(); h_dir.release();
         for (auto& b : xspill) b.release();
-        pk_host.release(); pk_dev.release(); h_xsl.release(); xsl.release();
+        pk_host.release(); pk_dev.release(); h_xsl.release(); xsl.release(); xtime.release();
         if (st) { cudaSetDevice(dev); cudaStreamDestroy(st); }
         for (int k = 1; k < kComputeStreams; ++k) if (xs[k]) cudaStreamDestroy(xs[k]);
         if (cst) cudaStreamDestroy(cst);
@@ -689,6 +689,7 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     a.xflags = nullptr;
     a.meta = nullptr;
     a.xs_skip = 0;
+    a.xtime = nullptr;
     a.hdr = s.hdr.as<ChunkHdr>();
     a.steps = s.steps.as<uint8_t>();
     a.frames = s.frames.as<float2>();
@@ -769,6 +770,11 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
         ag.pool = pool;
         ag.queue = s.counters.as<uint32_t>() + kQueueBase;
         ag.xs_skip = std::getenv("LTGP_XS_SKIP") ? (uint32_t)std::atoi(std::getenv("LTGP_XS_SKIP")) : 0u;
+        if (trace_slices()) {  // device timestamps of each slice's phases
+            TRY(s.xtime.ensure(8 * (1 + 3 * kMaxSlices), s.dev));
+            CK(cudaMemsetAsync(s.xtime.p, 0, 8 * (1 + 3 * kMaxSlices), s.st));
+            ag.xtime = s.xtime.as<unsigned long long>();
+        }
         K_EVAL_XS<<<s.eval_grid, kWarps * 32, eval_smem_bytes(), s.st>>>(ag, e->suite);
         CK(cudaGetLastError());
         ++launches;
@@ -1628,6 +1634,13 @@ int ltgp_evaluate_packed(ltgp_engine* e, uint32_t M, const uint8_t* buf, uint64_
                              s.slices[g].len / 1e6,
                              (g + 1 < s.slices.size() ? s.slices[g + 1].tree_begin : s.count) - s.slices[g].tree_begin,
                              t[0], t[1], t[2]);
+            }
+            if (s.xtime.p) {  // cross-slice launch: device time of each slice's phases after the launch began
+                std::vector<unsigned long long> xt(1 + 3 * kMaxSlices);
+                CK(cudaMemcpy(xt.data(), s.xtime.p, 8 * xt.size(), cudaMemcpyDeviceToHost));
+                for (size_t g = 0; g < s.slices.size(); ++g)
+                    std::fprintf(stderr, "  xs slice %2zu: decoded %7.3f planned %7.3f evaluated %7.3f (ms after launch)\n", g,
+                                 (xt[1 + 3 * g] - xt[0]) * 1e-6, (xt[2 + 3 * g] - xt[0]) * 1e-6, (xt[3 + 3 * g] - xt[0]) * 1e-6);
             }
         }
         s.slices.clear();
