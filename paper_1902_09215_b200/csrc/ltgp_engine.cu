@@ -8,6 +8,7 @@
 
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <sched.h>
 #include <nvtx3/nvToolsExt.h>
 #include <nccl.h>  // types only: libnccl is opened at run time (see RecordGather)
 
@@ -217,10 +218,17 @@ bool pack_enabled() {
     const char* v = std::getenv("LTGP_PACK");
     return !v || std::atoi(v) != 0;
 }
-int pack_threads() {  // the calling thread launches the slices' kernels meanwhile: one core for it
+int pack_threads() {
     const char* v = std::getenv("LTGP_PACK_THREADS");
-    const int n = v ? std::atoi(v) : (int)std::thread::hardware_concurrency() - 1;
-    return std::max(1, std::min(n, 256));
+    if (v) return std::max(1, std::min(std::atoi(v), 256));
+    // the CPUs this process may run on, shared with the other ranks of a
+    // one-process-per-GPU launch (torchrun sets LOCAL_WORLD_SIZE): spinning
+    // packers must never outnumber the cores. One core stays with the
+    // calling thread (it launches kernels, or packs a share itself).
+    cpu_set_t cs;
+    int n = sched_getaffinity(0, sizeof cs, &cs) == 0 ? CPU_COUNT(&cs) : (int)std::thread::hardware_concurrency();
+    if (const char* w = std::getenv("LOCAL_WORLD_SIZE")) n /= std::max(1, std::atoi(w));
+    return std::max(1, std::min(n - 1, 256));
 }
 constexpr uint32_t kQueueBase = 16;    // counters[16 + g]: work queue of slice g
 constexpr uint32_t kPoolCounters = 8;  // counters[8..11]: chunk-summary pool claims (2 x u64)
