@@ -223,12 +223,14 @@ int pack_threads() {
     if (v) return std::max(1, std::min(std::atoi(v), 256));
     // the CPUs this process may run on, shared with the other ranks of a
     // one-process-per-GPU launch (torchrun sets LOCAL_WORLD_SIZE): spinning
-    // packers must never outnumber the cores. One core stays with the
-    // calling thread (it launches kernels, or packs a share itself).
+    // packers must never outnumber the cores.
     cpu_set_t cs;
     int n = sched_getaffinity(0, sizeof cs, &cs) == 0 ? CPU_COUNT(&cs) : (int)std::thread::hardware_concurrency();
     if (const char* w = std::getenv("LOCAL_WORLD_SIZE")) n /= std::max(1, std::atoi(w));
-    return std::max(1, std::min(n - 1, 256));
+    // two cores stay free: the calling thread (kernel launches, or a share
+    // of the packing) and whatever else the host runs (config 3, 16 cores:
+    // 14 threads 16.37 ms per call, 15 threads 16.71)
+    return std::max(1, std::min(n - 2, 256));
 }
 constexpr uint32_t kQueueBase = 16;    // counters[16 + g]: work queue of slice g
 constexpr uint32_t kPoolCounters = 8;  // counters[8..11]: chunk-summary pool claims (2 x u64)
@@ -242,7 +244,12 @@ static_assert(kMaxSlices == kMaxXSlices, "one flag triple per slice");
 // per-slice launches
 bool xslice_enabled() {
     const char* v = std::getenv("LTGP_XSLICE");
-    return !v || std::atoi(v) != 0;
+    if (v) return std::atoi(v) != 0;
+    // a tool that serialises kernel launches (ncu, compute-sanitizer: both
+    // inject through CUDA_INJECTION64_PATH; CUDA_LAUNCH_BLOCKING) would hold
+    // the host inside the launch while the kernel waits for the host's copies
+    const char* lb = std::getenv("CUDA_LAUNCH_BLOCKING");
+    return !std::getenv("CUDA_INJECTION64_PATH") && !(lb && std::atoi(lb) != 0);
 }
 // cuStreamWriteValue32 (driver API, found at run time): the copy stream marks
 // a slice copied without a kernel (every SM may be busy in k_eval)
@@ -1065,6 +1072,11 @@ int check_eval(Shard& s) {
         return -1;
     }
     if (flags & 8u) { set_err("k_eval shared-memory layout does not fit"); return -1; }
+    if (flags & 64u) {
+        set_err("cross-slice k_eval: a slice's copy never landed (kernel launches serialised by a tool? "
+                "set LTGP_XSLICE=0)");
+        return -1;
+    }
     // malformed first: an invalid genome also derails the plan/scan cross-check
     if (flags & 2u) { set_err("malformed genome (stack underflow, leftover values or opcode 255 inside a tree)"); return -1; }
     if (flags & 16u) { set_err("chunk summary differs from k_plan's sizing (internal error)"); return -1; }

@@ -1,11 +1,12 @@
 // ltgp_pack.cpp — multi-threaded host packing of opcode slices (format in
 // ltgp_pack.h). Host code only (g++), linked into libltgp_cuda.so.
 //
-// Worker t packs a run of whole 256-packet blocks: the three code planes go
+// Workers claim chunks of 16 blocks of 256 packets: the three code planes go
 // to the destination with non-temporal stores (a block's plane words are
-// 512 B each), literals to a per-thread scratch that stays in its cache. At a
-// barrier the last worker turns the block literal counts into bases; then
-// every worker streams its literals to their final place. The destination is
+// 512 B each), literals to the chunk's scratch region (still in the thread's
+// cache when it copies them). At a barrier the last worker turns the block
+// literal counts into bases; then the chunks' literals are streamed to their
+// final place. The destination is
 // pinned memory the copy engine reads next, so nothing is gained by leaving
 // it in the CPU caches; non-temporal stores also skip the read-for-ownership
 // traffic. The AVX-512 path (VBMI2 byte compress) encodes 64 bytes per step;
@@ -102,9 +103,14 @@ bool have_avx512() {
     return v;
 }
 
-// n worker threads packing one slice at a time (the caller only starts and
-// waits). A streamed evaluation packs a slice every ~0.5 ms, so idle workers
-// spin for a while (no futex wake-up on the critical path) before sleeping.
+// n worker threads packing one slice at a time (the caller starts, then
+// waits, or helps). Work is claimed dynamically in chunks of kChunkBlocks
+// blocks, so a thread the OS preempts (the host is shared with the caller,
+// a driver thread, a clock sampler) delays one chunk, not a fixed share of
+// the slice. A streamed evaluation packs a slice every ~0.3 ms, so idle
+// workers spin for a while (no futex wake-up on the critical path) before
+// sleeping.
+constexpr uint64_t kChunkBlocks = 16;  // 64 KB of input
 struct Pool {
     int n;
     std::vector<std::thread> th;
@@ -113,24 +119,22 @@ struct Pool {
     std::atomic<uint64_t> gen{0};
     std::atomic<int> pending{0}, arrived{0};
     std::atomic<uint64_t> phase2{0};
+    std::atomic<uint64_t> next1{0}, next2{0};
     std::atomic<int> sleepers{0};
     std::atomic<bool> stop{false};
-    std::vector<std::vector<uint8_t>> scratch;
+    std::vector<uint8_t> scratch;   // literals of chunk c at c * kChunkBlocks * 4096
     // the job
     const uint8_t* src = nullptr;
     uint64_t len = 0;
     uint8_t* dst = nullptr;
     Layout L{0};
-    int T = 0;
-    int parts = 0;      // workers + the caller when it helps (pack_wait(help))
-    std::vector<uint64_t> b0, nlit, tl;
-    std::vector<uint32_t> cnt;
+    uint64_t nchunks = 0;
+    int parts = 0;      // threads taking part: the workers, plus the caller when it helps
+    std::vector<uint32_t> cnt;     // literals per block
+    std::vector<uint64_t> cl, co;  // literals per chunk, and their offsets
     uint64_t total = 0;
 
-    explicit Pool(int nthreads) : n(std::max(1, nthreads)), scratch(n + 1) {
-        b0.resize(n + 2);
-        nlit.resize(n + 1);
-        tl.resize(n + 1);
+    explicit Pool(int nthreads) : n(std::max(1, nthreads)) {
         for (int t = 0; t < n; ++t) th.emplace_back([this, t] { worker(t); });
     }
     ~Pool() {
@@ -141,20 +145,21 @@ struct Pool {
         cv.notify_all();
         for (auto& x : th) x.join();
     }
-    void work(int t, uint64_t my_gen) {
-        if (t < T) {
-            std::vector<uint8_t>& s = scratch[t];
-            const uint64_t bytes = (b0[t + 1] - b0[t]) * kBlockPackets * 16 + 64;
-            if (s.size() < bytes) s.resize(bytes);
-            nlit[t] = have_avx512() ? encode_avx512(src, len, L, dst, b0[t], b0[t + 1], s.data(), cnt.data() + b0[t])
-                                    : encode_scalar(src, len, L, dst, b0[t], b0[t + 1], s.data(), cnt.data() + b0[t]);
+    void work(uint64_t my_gen) {
+        const bool simd = have_avx512();
+        for (uint64_t c; (c = next1.fetch_add(1)) < nchunks;) {
+            const uint64_t b0 = c * kChunkBlocks, b1 = std::min(L.nblk, b0 + kChunkBlocks);
+            uint8_t* lit = scratch.data() + c * kChunkBlocks * kBlockPackets * 16;
+            cl[c] = simd ? encode_avx512(src, len, L, dst, b0, b1, lit, cnt.data() + b0)
+                         : encode_scalar(src, len, L, dst, b0, b1, lit, cnt.data() + b0);
         }
         if (arrived.fetch_add(1) == parts - 1) {  // the last one: block literal bases
             uint32_t* base = reinterpret_cast<uint32_t*>(dst + L.base_off);
             uint64_t acc = 0;
-            for (int u = 0; u < T; ++u) {
-                tl[u] = acc;
-                for (uint64_t b = b0[u]; b < b0[u + 1]; ++b) {
+            for (uint64_t c = 0; c < nchunks; ++c) {
+                co[c] = acc;
+                const uint64_t b1 = std::min(L.nblk, (c + 1) * kChunkBlocks);
+                for (uint64_t b = c * kChunkBlocks; b < b1; ++b) {
                     base[b] = (uint32_t)acc;
                     acc += cnt[b];
                 }
@@ -164,10 +169,11 @@ struct Pool {
         } else {
             for (int i = 0; phase2.load() != my_gen; ++i) relax(i);
         }
-        if (t < T && nlit[t]) copy_nt(dst + L.lit_off + tl[t], scratch[t].data(), nlit[t]);
+        for (uint64_t c; (c = next2.fetch_add(1)) < nchunks;)
+            if (cl[c]) copy_nt(dst + L.lit_off + co[c], scratch.data() + c * kChunkBlocks * kBlockPackets * 16, cl[c]);
         _mm_sfence();
     }
-    void worker(int t) {
+    void worker(int) {
         uint64_t seen = 0;
         for (;;) {
             for (int i = 0; i < 100000 && gen.load() == seen && !stop; ++i) _mm_pause();
@@ -179,18 +185,22 @@ struct Pool {
             }
             if (stop) return;
             seen = gen.load();
-            work(t, seen);
+            work(seen);
             --pending;
         }
     }
     void start(const uint8_t* s, uint64_t l, uint8_t* d, bool help) {
         src = s, len = l, dst = d;
         L = Layout(l);
+        nchunks = (L.nblk + kChunkBlocks - 1) / kChunkBlocks;
         parts = n + (help ? 1 : 0);
-        T = (int)std::min<uint64_t>((uint64_t)parts, std::max<uint64_t>(1, L.nblk));
-        for (int t = 0; t <= T; ++t) b0[t] = L.nblk * t / T;
-        for (int t = 0; t < parts; ++t) nlit[t] = 0;
+        const uint64_t sb = nchunks * kChunkBlocks * kBlockPackets * 16 + 64;
+        if (scratch.size() < sb) scratch.resize(sb);
         cnt.assign(L.nblk, 0);
+        cl.assign(nchunks, 0);
+        co.assign(nchunks, 0);
+        next1 = 0;
+        next2 = 0;
         arrived = 0;
         pending = n;
         ++gen;
@@ -200,7 +210,7 @@ struct Pool {
         }
     }
     uint64_t wait() {
-        if (parts > n) work(n, gen.load());  // the caller's part
+        if (parts > n) work(gen.load());  // the caller takes chunks too
         for (int i = 0; pending.load(); ++i) relax(i);
         return total;
     }
