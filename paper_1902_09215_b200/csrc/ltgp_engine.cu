@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <sched.h>
+#include <unistd.h>  // environ
 #include <nvtx3/nvToolsExt.h>
 #include <nccl.h>  // types only: libnccl is opened at run time (see RecordGather)
 
@@ -245,11 +246,18 @@ static_assert(kMaxSlices == kMaxXSlices, "one flag triple per slice");
 bool xslice_enabled() {
     const char* v = std::getenv("LTGP_XSLICE");
     if (v) return std::atoi(v) != 0;
-    // a tool that serialises kernel launches (ncu, compute-sanitizer: both
-    // inject through CUDA_INJECTION64_PATH; CUDA_LAUNCH_BLOCKING) would hold
-    // the host inside the launch while the kernel waits for the host's copies
+    // a tool that serialises kernel launches (ncu: NV_NSIGHT_INJECTION_* /
+    // NV_COMPUTE_PROFILER_*; injection libraries: CUDA_INJECTION64_PATH;
+    // compute-sanitizer; CUDA_LAUNCH_BLOCKING) would hold the host inside the
+    // launch while the kernel waits for the host's copies
     const char* lb = std::getenv("CUDA_LAUNCH_BLOCKING");
-    return !std::getenv("CUDA_INJECTION64_PATH") && !(lb && std::atoi(lb) != 0);
+    if (lb && std::atoi(lb) != 0) return false;
+    for (char** e = environ; e && *e; ++e)
+        if (!std::strncmp(*e, "NV_NSIGHT_INJECTION", 19) || !std::strncmp(*e, "NV_COMPUTE_PROFILER", 19) ||
+            !std::strncmp(*e, "CUDA_INJECTION64_PATH=", 22) || !std::strncmp(*e, "NV_SANITIZER", 12) ||
+            !std::strncmp(*e, "COMPUTE_SANITIZER", 17))
+            return false;
+    return true;
 }
 // cuStreamWriteValue32 (driver API, found at run time): the copy stream marks
 // a slice copied without a kernel (every SM may be busy in k_eval)
