@@ -187,7 +187,6 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
 
     import paper_1902_09215_b200 as ltgp
-    from paper_1902_09215_b200.sharding import DeviceRecords
 
     torch.cuda.set_device(local_rank)
     pk, pk_kind = peaks()
@@ -214,15 +213,17 @@ def run_ours(args, rank, world, local_rank):
     rec = np.zeros(count, ltgp.RECORD_DTYPE)
     dptr, _, _, sptr = e.shard_records(0)
     estream = torch.cuda.ExternalStream(sptr)
-    cmax = max(c for _, c in ranges)
-    gather_out = torch.empty(world * cmax * 16, dtype=torch.uint8, device="cuda")
-    gather_in = torch.zeros(cmax * 16, dtype=torch.uint8, device="cuda")
+    if world > 1:
+        # the engine joins the ranks' NCCL communicator (ltgp_nccl_attach):
+        # every evaluation then all-gathers the ranks' records inside the
+        # engine (one ncclAllGather over NVLink; the tournament-selection
+        # exchange), the same code the run loop's record gather uses
+        uid = [ltgp.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        e.nccl_attach(uid[0], world, rank)
 
     def gather():
-        if world > 1:  # records of every shard to every rank (NCCL over NVLink)
-            dev_rec = torch.as_tensor(DeviceRecords(dptr, count), device="cuda")
-            gather_in[: count * 16].copy_(dev_rec)
-            dist.all_gather_into_tensor(gather_out, gather_in)
+        pass  # inside evaluate_collect / evaluate_packed (the engine's all-gather)
 
     def step(host_records=True):
         e.evaluate_launch()
@@ -337,6 +338,12 @@ def run_ours(args, rank, world, local_rank):
                      "combine_ms": float(np.mean(comb)) * 1e3, "binding": binding},
         "clocks": clk,
     }
+    if world > 1:
+        g = e.gathered_records()
+        ok = g.size == world * count and g[rank * count:(rank + 1) * count].tobytes() == rec.tobytes()
+        line["collective"] = {"impl": e.gather_mode(), "op": "ncclAllGather of the 16-byte records every step",
+                              "nranks": world, "gather_ms": e.stats()["gather_seconds"] * 1e3,
+                              "own_block_matches": bool(ok)}
     if world == 1 and rank == 0 and not args.no_evolution:
         # secondary: BASELINE configs[1] (pop 4000, k=7, crossover only, no size
         # limit, 200 generations, bloating 50/50-grow variant — see DESIGN.md

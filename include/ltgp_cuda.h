@@ -69,7 +69,8 @@ typedef struct {
     uint64_t last_window_adjusts; /* of which needed a stack window spill or refill */
     uint64_t last_spine_steps;  /* spine steps the chunk summaries of the last evaluation hold */
     uint32_t kernel_launches;   /* engine kernels launched by the last call */
-    uint32_t gather_nccl;       /* 1: records are all-gathered by NCCL (distinct devices, use_nccl) */
+    uint32_t gather_nccl;       /* 1: records are all-gathered by NCCL (distinct devices, use_nccl);
+                                   2: across processes (ltgp_nccl_attach) */
     double keval_seconds;       /* k_eval alone, max over shards (resident evaluations; 0 when streamed) */
     uint64_t live_genomes_high_water; /* streaming memory mode: most live genomes (parents not yet
                                          retired + children built) seen at a wave boundary */
@@ -210,6 +211,18 @@ uint32_t ltgp_population_size(ltgp_engine* e);
    callers that run their own collective (e.g. torch.distributed NCCL). */
 int ltgp_shard_records(ltgp_engine* e, int s, void** dev_records, uint32_t* first,
                        uint32_t* count, void** stream);
+
+/* One process per GPU (torchrun / bench.py --gpus N): the engine (one shard)
+   joins an NCCL communicator across processes and every evaluation
+   all-gathers the ranks' 16-byte records (tournament selection needs every
+   fitness), over NVLink. ltgp_nccl_unique_id makes the
+   communicator id on one rank (128 bytes, to be broadcast by the caller);
+   ltgp_nccl_attach joins with it (equal population sizes per rank);
+   ltgp_gathered_records returns the last gather: nranks x M records, rank r's
+   at r x M (*n = their count; out may be NULL to query it). */
+int ltgp_nccl_unique_id(uint8_t* out128);
+int ltgp_nccl_attach(ltgp_engine* e, const uint8_t* id128, int nranks, int rank);
+int ltgp_gathered_records(ltgp_engine* e, ltgp_record* out, uint32_t cap, uint32_t* n);
 
 /* The packed form a streamed evaluation sends over PCIe (ltgp_pack.h:
    3-bit codes for opcodes 0-4 and 0xFF, literal bytes for the rest), exposed

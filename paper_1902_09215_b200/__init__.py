@@ -94,6 +94,9 @@ _CUDA_SIGS = {
     "ltgp_population_size": (C.c_uint32, [_P]),
     "ltgp_shard_records": (C.c_int, [_P, C.c_int, C.POINTER(_P), C.POINTER(C.c_uint32),
                                      C.POINTER(C.c_uint32), C.POINTER(_P)]),
+    "ltgp_nccl_unique_id": (C.c_int, [_P]),
+    "ltgp_nccl_attach": (C.c_int, [_P, _P, C.c_int, C.c_int]),
+    "ltgp_gathered_records": (C.c_int, [_P, _P, C.c_uint32, C.POINTER(C.c_uint32)]),
     "ltgp_pack_bound": (C.c_uint64, [C.c_uint64]),
     "ltgp_pack_host": (C.c_uint64, [_P, C.c_uint64, _P, C.c_int]),
 }
@@ -164,6 +167,14 @@ def _err():
 def _check(status):
     if status != 0:
         raise EngineError(_err())
+
+
+def nccl_unique_id() -> bytes:
+    """A communicator id for Engine.nccl_attach (made on one rank, broadcast
+    by the caller)."""
+    buf = np.zeros(128, np.uint8)
+    _check(cuda_lib().ltgp_nccl_unique_id(_ptr(buf)))
+    return buf.tobytes()
 
 
 def pack_host(buf: np.ndarray, threads: int = 1) -> np.ndarray:
@@ -449,11 +460,28 @@ class Engine:
         _check(self._lib.ltgp_get_stats(self._h, C.byref(st)))
         return {k: getattr(st, k) for k, _ in _Stats._fields_}
 
+    def nccl_attach(self, uid: bytes, nranks: int, rank: int):
+        """One process per GPU: join the ranks' NCCL communicator; every
+        evaluation then all-gathers the ranks' records (gathered_records)."""
+        ub = np.frombuffer(uid, np.uint8).copy()
+        _check(self._lib.ltgp_nccl_attach(self._h, _ptr(ub), nranks, rank))
+
+    def gathered_records(self) -> np.ndarray:
+        n = C.c_uint32(0)
+        _check(self._lib.ltgp_gathered_records(self._h, None, 0, C.byref(n)))
+        out = np.zeros(n.value, RECORD_DTYPE)
+        _check(self._lib.ltgp_gathered_records(self._h, _ptr(out), n.value, C.byref(n)))
+        return out
+
     def gather_mode(self) -> str:
         """How multi-shard records are all-gathered: "nccl" (distinct devices,
         one grouped ncclAllGather), "copies" (peer copies to shard 0: shards
-        that repeat a device) or "none" (one shard)."""
-        if self.stats()["gather_nccl"]:
+        that repeat a device), "nccl-processes" (ltgp_nccl_attach: one
+        process per GPU) or "none" (one shard)."""
+        g = self.stats()["gather_nccl"]
+        if g == 2:
+            return "nccl-processes"
+        if g:
             return "nccl"
         return "copies" if len(self.devices) > 1 else "none"
 

@@ -399,9 +399,17 @@ struct ltgp_engine {
         ncclResult_t (*group_end)() = nullptr;
         ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
         const char* (*error_string)(ncclResult_t) = nullptr;
+        ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
         DevBuf send[LTGP_MAX_SHARDS], recv[LTGP_MAX_SHARDS];  // NCCL: per shard; copies: recv[0] only
         HostBuf h;
         cudaEvent_t ev[2] = {};
+        // one process per GPU (ltgp_nccl_attach): this engine is one rank of
+        // a communicator across processes; every evaluation all-gathers the
+        // ranks' records (rank r's block at r x count)
+        bool mp = false;
+        int mp_rank = 0, mp_nranks = 1;
+        ncclComm_t mp_comm = nullptr;
+        uint32_t mp_count = 0;  // records per rank of the last gather
     } gather;
 };
 
@@ -1160,6 +1168,27 @@ int upload_tables(Shard& s, TreeSet& ts) {
     return 0;
 }
 
+// libnccl.so.2, opened at run time with RTLD_LOCAL (torch may have loaded
+// its own copy into the process; its soname resolves to that copy)
+int open_nccl(ltgp_engine::Gather& g) {
+    if (g.lib) return 0;
+    g.lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!g.lib) { set_err("cannot open libnccl.so.2: %s", dlerror()); return -1; }
+    g.comm_init_all = reinterpret_cast<decltype(g.comm_init_all)>(dlsym(g.lib, "ncclCommInitAll"));
+    g.comm_init_rank = reinterpret_cast<decltype(g.comm_init_rank)>(dlsym(g.lib, "ncclCommInitRank"));
+    g.all_gather = reinterpret_cast<decltype(g.all_gather)>(dlsym(g.lib, "ncclAllGather"));
+    g.group_start = reinterpret_cast<decltype(g.group_start)>(dlsym(g.lib, "ncclGroupStart"));
+    g.group_end = reinterpret_cast<decltype(g.group_end)>(dlsym(g.lib, "ncclGroupEnd"));
+    g.comm_destroy = reinterpret_cast<decltype(g.comm_destroy)>(dlsym(g.lib, "ncclCommDestroy"));
+    g.error_string = reinterpret_cast<decltype(g.error_string)>(dlsym(g.lib, "ncclGetErrorString"));
+    if (!g.comm_init_all || !g.comm_init_rank || !g.all_gather || !g.group_start || !g.group_end ||
+        !g.comm_destroy || !g.error_string) {
+        set_err("libnccl.so.2 lacks a required symbol");
+        return -1;
+    }
+    return 0;
+}
+
 // Opens NCCL for a population sharded over distinct devices (cfg.use_nccl):
 // one communicator per shard, created in-process by ncclCommInitAll. The
 // library is opened at run time with RTLD_LOCAL (torch may have loaded its
@@ -1175,18 +1204,7 @@ int init_gather(ltgp_engine* e) {
         for (int j = 0; j < i; ++j)
             if (e->shards[i].dev == e->shards[j].dev) distinct = false;
     if (!e->cfg.use_nccl || !distinct) return 0;
-    g.lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
-    if (!g.lib) { set_err("use_nccl: cannot open libnccl.so.2: %s", dlerror()); return -1; }
-    g.comm_init_all = reinterpret_cast<decltype(g.comm_init_all)>(dlsym(g.lib, "ncclCommInitAll"));
-    g.all_gather = reinterpret_cast<decltype(g.all_gather)>(dlsym(g.lib, "ncclAllGather"));
-    g.group_start = reinterpret_cast<decltype(g.group_start)>(dlsym(g.lib, "ncclGroupStart"));
-    g.group_end = reinterpret_cast<decltype(g.group_end)>(dlsym(g.lib, "ncclGroupEnd"));
-    g.comm_destroy = reinterpret_cast<decltype(g.comm_destroy)>(dlsym(g.lib, "ncclCommDestroy"));
-    g.error_string = reinterpret_cast<decltype(g.error_string)>(dlsym(g.lib, "ncclGetErrorString"));
-    if (!g.comm_init_all || !g.all_gather || !g.group_start || !g.group_end || !g.comm_destroy || !g.error_string) {
-        set_err("use_nccl: libnccl.so.2 lacks a required symbol");
-        return -1;
-    }
+    TRY(open_nccl(g));
     int devs[LTGP_MAX_SHARDS];
     for (int i = 0; i < n; ++i) devs[i] = e->shards[i].dev;
     const ncclResult_t r = g.comm_init_all(g.comms, n, devs);
@@ -1203,6 +1221,7 @@ void release_gather(ltgp_engine* e) {
     auto& g = e->gather;
     if (g.nccl)
         for (size_t i = 0; i < e->shards.size(); ++i) g.comm_destroy(g.comms[i]);
+    if (g.mp && g.mp_comm) g.comm_destroy(g.mp_comm);
     for (auto& b : g.send) b.release();
     for (auto& b : g.recv) b.release();
     g.h.release();
@@ -1275,6 +1294,30 @@ int gather_records(ltgp_engine* e, ltgp_record* out) {
     return 0;
 }
 
+// One process per GPU (ltgp_nccl_attach): the ranks' records to every rank,
+// one ncclAllGather over the engine's own communicator. Ranks must hold equal
+// population sizes (a one-process-per-GPU batch: N config-3 batches).
+int gather_records_mp(ltgp_engine* e) {
+    NvtxRange nr("ltgp.record_all_gather");
+    auto& g = e->gather;
+    Shard& s = e->shards[0];
+    const size_t blk = sizeof(ltgp_record) * std::max<uint32_t>(s.count, 1);
+    CK(cudaSetDevice(s.dev));
+    TRY(g.recv[0].ensure(blk * g.mp_nranks, s.dev));
+    CK(cudaEventRecord(g.ev[0], s.st));
+    const ncclResult_t r = g.all_gather(s.rec.p, g.recv[0].p, blk, ncclUint8, g.mp_comm, s.st);
+    if (r != ncclSuccess) { set_err("ncclAllGather: %s", g.error_string(r)); return -1; }
+    CK(cudaEventRecord(g.ev[1], s.st));
+    TRY(g.h.ensure(blk * g.mp_nranks));
+    CK(cudaMemcpyAsync(g.h.p, g.recv[0].p, blk * g.mp_nranks, cudaMemcpyDeviceToHost, s.st));
+    CK(cudaStreamSynchronize(s.st));
+    float ms = 0.0f;
+    CK(cudaEventElapsedTime(&ms, g.ev[0], g.ev[1]));
+    e->stats.gather_seconds = ms * 1e-3;
+    g.mp_count = s.count;
+    return 0;
+}
+
 int collect(ltgp_engine* e, ltgp_record* out, float* outs48) {
     double secs = 0.0, ksecs = 0.0, csecs = 0.0, kev = 0.0;
     uint64_t nodes = 0, chunks = 0, reruns = 0, exits = 0, adjusts = 0, steps = 0;
@@ -1312,6 +1355,7 @@ int collect(ltgp_engine* e, ltgp_record* out, float* outs48) {
         steps += s.last_steps;
     }
     if (e->shards.size() > 1) TRY(gather_records(e, out));
+    else if (e->gather.mp) TRY(gather_records_mp(e));
     e->stats.last_spine_steps = steps;
     e->stats.last_exits = exits;
     e->stats.last_window_adjusts = adjusts;
@@ -1681,6 +1725,55 @@ int ltgp_evaluate_packed(ltgp_engine* e, uint32_t M, const uint8_t* buf, uint64_
     return collect(e, out, outs48);
 }
 
+int ltgp_nccl_unique_id(uint8_t* out128) {
+    if (!out128) { set_err("null argument"); return -1; }
+    static ltgp_engine::Gather g;  // the library only
+    TRY(open_nccl(g));
+    auto get_id = reinterpret_cast<ncclResult_t (*)(ncclUniqueId*)>(dlsym(g.lib, "ncclGetUniqueId"));
+    if (!get_id) { set_err("libnccl.so.2 lacks ncclGetUniqueId"); return -1; }
+    ncclUniqueId id;
+    const ncclResult_t r = get_id(&id);
+    if (r != ncclSuccess) { set_err("ncclGetUniqueId: %s", g.error_string(r)); return -1; }
+    static_assert(sizeof(ncclUniqueId) == 128, "NCCL_UNIQUE_ID_BYTES");
+    std::memcpy(out128, &id, 128);
+    return 0;
+}
+
+int ltgp_nccl_attach(ltgp_engine* e, const uint8_t* id128, int nranks, int rank) {
+    if (!e || !id128) { set_err("null argument"); return -1; }
+    if (e->shards.size() != 1) { set_err("ltgp_nccl_attach: one shard (one GPU) per process"); return -1; }
+    if (nranks < 1 || rank < 0 || rank >= nranks) { set_err("ltgp_nccl_attach: rank %d of %d", rank, nranks); return -1; }
+    auto& g = e->gather;
+    if (g.mp) { set_err("ltgp_nccl_attach: already attached"); return -1; }
+    TRY(open_nccl(g));
+    ncclUniqueId id;
+    std::memcpy(&id, id128, 128);
+    CK(cudaSetDevice(e->shards[0].dev));
+    const ncclResult_t r = g.comm_init_rank(&g.mp_comm, nranks, id, rank);
+    if (r != ncclSuccess) { set_err("ncclCommInitRank: %s", g.error_string(r)); return -1; }
+    g.mp = true;
+    g.mp_rank = rank;
+    g.mp_nranks = nranks;
+    std::fprintf(stderr, "[ltgp] NCCL record all-gather across processes: ncclCommInitRank nranks=%d rank=%d device=%d\n",
+                 nranks, rank, e->shards[0].dev);
+    return 0;
+}
+
+int ltgp_gathered_records(ltgp_engine* e, ltgp_record* out, uint32_t cap, uint32_t* n) {
+    if (!e || !n) { set_err("null argument"); return -1; }
+    const auto& g = e->gather;
+    if (!g.mp) { set_err("ltgp_gathered_records: not attached (ltgp_nccl_attach)"); return -1; }
+    const uint32_t total = g.mp_count * (uint32_t)g.mp_nranks;
+    *n = total;
+    if (out) {
+        if (cap < total) { set_err("ltgp_gathered_records: %u records, room for %u", total, cap); return -1; }
+        const size_t blk = sizeof(ltgp_record) * std::max<uint32_t>(g.mp_count, 1);
+        for (int r = 0; r < g.mp_nranks; ++r)
+            std::memcpy(out + (size_t)r * g.mp_count, g.h.as<uint8_t>() + blk * r, sizeof(ltgp_record) * g.mp_count);
+    }
+    return 0;
+}
+
 uint64_t ltgp_pack_bound(uint64_t len) { return ltgp_pack::Layout(len).max_bytes(); }
 
 uint64_t ltgp_pack_host(const uint8_t* src, uint64_t len, uint8_t* dst, int threads) {
@@ -1738,7 +1831,7 @@ int ltgp_get_stats(ltgp_engine* e, ltgp_stats* out) {
     for (Shard& s : e->shards)
         for (auto& ts : s.set) hw = std::max<uint64_t>(hw, ts.arena.bytes);
     e->stats.arena_high_water = hw;
-    e->stats.gather_nccl = e->gather.nccl ? 1u : 0u;
+    e->stats.gather_nccl = e->gather.mp ? 2u : e->gather.nccl ? 1u : 0u;
     e->stats.live_genomes_high_water = e->live_high_water;
     e->stats.arena_used_high_water = e->used_high_water;
     *out = e->stats;

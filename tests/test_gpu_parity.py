@@ -873,3 +873,41 @@ def test_streaming_memory_mode(oracle, suite, tmp_path):
         assert e.stats()["live_genomes_high_water"] < 2 * 400
     assert g["generations"] == r["generations"] and g["nodes"] == r["nodes"]
     assert d.read_bytes() == ref.read_bytes()
+
+
+def test_nccl_attach_one_rank(oracle, suite):
+    """One process per GPU (ltgp_nccl_attach, bench.py --gpus N): a
+    single-rank communicator across processes; every evaluation all-gathers
+    the records inside the engine, equal to the records."""
+    buf, offs, sizes = ltgp.corpus(3, 60, 3.0, 4.5)
+    uid = ltgp.nccl_unique_id()
+    with engine(suite) as e:
+        e.nccl_attach(uid, 1, 0)
+        assert e.gather_mode() == "nccl-processes"
+        e.upload_packed(buf, offs, sizes)
+        rec = e.evaluate_population()
+        assert e.gathered_records().tobytes() == rec.tobytes()
+        rec2 = e.evaluate_packed(buf, offs, sizes)
+        assert e.gathered_records().tobytes() == rec2.tobytes() == rec.tobytes()
+        with pytest.raises(ltgp.EngineError):
+            e.nccl_attach(uid, 1, 0)  # already attached
+    assert_records_equal(rec, oracle.evaluate_population(buf, offs, sizes, suite, threads=0))
+
+
+@pytest.mark.skipif("_gpus() < 2")
+def test_bench_multi_gpu_engine_gather(tmp_path):
+    """bench.py --gpus 2 under torchrun (the SCALE run's launch): each rank's
+    engine all-gathers every rank's records through its own NCCL
+    communicator, and each rank's block is its own records."""
+    import subprocess
+    import sys
+    root = os.path.dirname(HERE)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(root, "bench.py"),
+           "--gpus", "2", "--steps", "2", "--warmup", "3", "--no-evolution", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2
+    assert line["collective"]["impl"] == "nccl-processes" and line["collective"]["own_block_matches"]
+    assert "ncclCommInitRank nranks=2" in out.stderr
