@@ -131,11 +131,12 @@ int ltgp_evaluate_outputs(ltgp_engine* e, ltgp_record* out, float* outs48);
 
 /* evaluate_population (evolve.hpp:108-109) on host genomes in one call:
    the packed buffer (same layout rules as ltgp_upload_packed) becomes the
-   population and is evaluated while it uploads. Slices of ~16 MB go
-   host-to-device on a copy stream and each slice's trees are evaluated as
-   soon as they land. Each slice is packed on the host first (ltgp_pack_host:
-   ~0.63 B per node instead of 1, host threads; LTGP_PACK=0 sends the raw
-   bytes) and rebuilt into the arena on the device. out: M records;
+   population and is evaluated while it uploads. The buffer goes over in
+   slices (16 MB target, at most 48), each packed on the host first
+   (ltgp_pack_host: ~0.63 B per node instead of 1, host threads;
+   LTGP_PACK=0 sends the raw bytes); one persistent kernel rebuilds, decodes,
+   plans and evaluates every slice as it lands (LTGP_XSLICE=0: per-slice
+   launches; also the case under launch-serialising tools). out: M records;
    outs48: per-case outputs or NULL. */
 int ltgp_evaluate_packed(ltgp_engine* e, uint32_t M, const uint8_t* buf, uint64_t buf_bytes,
                          const uint64_t* offsets, const uint64_t* sizes, ltgp_record* out,
