@@ -285,8 +285,8 @@ struct Shard {
     HostBuf pk_host;                            // packed slices (ltgp_pack.h), pinned, one region per slice
     DevBuf pk_dev;                              // and their device copies
     uint64_t h2d_bytes = 0;                     // bytes the last streamed evaluation sent
-    HostBuf h_xsl;                              // cross-slice launch: the slice descriptors (XSlice)
-    DevBuf xsl, xtime;                          // and its trace timestamps (LTGP_TRACE)
+    HostBuf h_xsl, h_xblk;                      // cross-slice launch: the slice descriptors (XSlice), task blocks
+    DevBuf xsl, xblk, xtime;                    // and its trace timestamps (LTGP_TRACE)
     std::vector<uint32_t> slice_items;          // slice g's items: [slice_items[g], slice_items[g+1])
     std::vector<uint32_t> slice_ct, slice_ch;   // slice g's chunked trees / chunks (same convention)
     std::vector<uint32_t> items_slices;         // work-list cache key (slice tree boundaries)
@@ -350,6 +350,7 @@ struct Shard {
         h_csize.release(); h_coff.release(); h_dir.release();
         for (auto& b : xspill) b.release();
         pk_host.release(); pk_dev.release(); h_xsl.release(); xsl.release(); xtime.release();
+        h_xblk.release(); xblk.release();
         if (st) { cudaSetDevice(dev); cudaStreamDestroy(st); }
         for (int k = 1; k < kComputeStreams; ++k) if (xs[k]) cudaStreamDestroy(xs[k]);
         if (cst) cudaStreamDestroy(cst);
@@ -468,6 +469,27 @@ int init_shard(ltgp_engine* e, Shard& s) {
 }
 
 int launch_combine(ltgp_engine* e, Shard& s, const CombineArgs& ca, cudaStream_t st, uint32_t& launches);
+
+// The cross-slice launch's queue: slice v's decode and plan tasks ahead of
+// slice v-1's eval tasks, so a slice's plans are done long before its first
+// eval task is taken (a plan barrier right in front of the evals idled the
+// warps between slices: an evolved population evaluated 40% slower).
+// Returns the task count; blocks = {first task, slice | kind << 16}.
+uint32_t xs_blocks(const XSlice* x, uint32_t G, std::vector<uint2>& blocks) {
+    blocks.clear();
+    uint32_t t = 0;
+    auto add = [&](uint32_t v, uint32_t kind, uint32_t n) {
+        if (n) blocks.push_back(make_uint2(t, v | kind << 16)), t += n;
+    };
+    for (uint32_t v = 0; v <= G; ++v) {
+        if (v < G) {
+            add(v, 0, x[v].nd);
+            add(v, 1, x[v].np);
+        }
+        if (v > 0) add(v - 1, 2, x[v - 1].np);
+    }
+    return t;
+}
 
 // Evaluate every tree of `ts` on shard s: records (and optional per-case
 // outputs) land in rec/outs. Asynchronous on s.st.
@@ -716,6 +738,8 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
     a.item_base = 0;
     a.xsl = nullptr;
     a.n_xs = 0;
+    a.xblk = nullptr;
+    a.n_xblk = 0;
     a.n_tasks = 0;
     a.xflags = nullptr;
     a.meta = nullptr;
@@ -791,10 +815,18 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             x.item0 = s.slice_items[g];
             task += x.nd + 2 * x.np;
         }
+        std::vector<uint2> blk;
+        task = xs_blocks(hx, G, blk);
+        TRY(s.h_xblk.ensure(sizeof(uint2) * blk.size()));
+        TRY(s.xblk.ensure(sizeof(uint2) * blk.size(), s.dev));
+        std::memcpy(s.h_xblk.p, blk.data(), sizeof(uint2) * blk.size());
+        CK(cudaMemcpyAsync(s.xblk.p, s.h_xblk.p, sizeof(uint2) * blk.size(), cudaMemcpyHostToDevice, s.st));
         CK(cudaMemcpyAsync(s.xsl.p, hx, sizeof(XSlice) * G, cudaMemcpyHostToDevice, s.st));
         EvalArgs ag = a;
         ag.xsl = s.xsl.as<XSlice>();
         ag.n_xs = G;
+        ag.xblk = s.xblk.as<uint2>();
+        ag.n_xblk = (uint32_t)blk.size();
         ag.n_tasks = task;
         ag.xflags = s.counters.as<uint32_t>() + kXFlagBase;
         ag.meta = ts.meta.as<uint32_t>();
