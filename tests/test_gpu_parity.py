@@ -197,6 +197,32 @@ def test_capacity_overflow_reruns(oracle, suite):
             assert rec["depth"][k] == oracle.depth(g)
 
 
+def test_streamed_capacity_overflow_reruns(oracle, suite, monkeypatch):
+    """The cross-slice launch (ltgp_evaluate_packed, several slices) hands
+    items that outgrow the spill area or the summary pool to the same re-run
+    tiers as a resident evaluation: records and outputs equal the resident
+    path's and the oracle's, with re-runs counted."""
+    gs = [ltgp.random_tree_of_size(31, 4999),
+          np.array([ADD] * 8000 + [X] + [5 + 7] * 8000, np.uint8),
+          ltgp.remy_tree(32, 20001),
+          np.array([SUB] * 5000 + [X] + [5 + (k % 250) for k in range(5000)], np.uint8),
+          ltgp.random_tree_of_size(33, 2999)]
+    buf, offs, sizes = pack(gs)
+    monkeypatch.setenv("LTGP_SLICE_KB", "8")
+    for chunk in (4096, 65536):
+        with engine(suite, chunk=chunk) as e:
+            rec, outs = e.evaluate_packed(buf, offs, sizes, outputs=True)
+            n = e.stats()["last_fallback_items"]
+            e.upload_packed(buf, offs, sizes)
+            ref, refo = e.evaluate_outputs()
+        assert n > 0, chunk
+        assert rec.tobytes() == ref.tobytes() and same_bits(outs, refo)
+        for k, g in enumerate(gs):
+            o, _ = oracle.eval_batch(g, suite[0], suite[2])
+            assert same_bits(outs[k], o)
+            assert rec["depth"][k] == oracle.depth(g)
+
+
 def test_subtree_extents(oracle, suite):
     genomes = [ltgp.remy_tree(7, 4001), ltgp.random_tree_of_size(8, 999), np.array([X], np.uint8)]
     with engine(suite) as e:
