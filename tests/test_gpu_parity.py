@@ -600,10 +600,11 @@ def test_config4_regime_large_remy_trees(oracle, suite):
 
 
 @pytest.mark.parametrize("round_", range(int(os.environ.get("LTGP_FUZZ_ROUNDS", "3"))))
-def test_randomized_populations(oracle, suite, round_):
+def test_randomized_populations(oracle, suite, round_, monkeypatch):
     """Randomized sweep: mixed shapes (Remy, uniform splits, ramped
     half-and-half, left/right chains), random sizes and chunk lengths, the
-    resident and the streamed path; every record and per-case output equal
+    resident and the streamed path (random slice sizes: one slice, or several
+    through the cross-slice launch); every record and per-case output equal
     to the oracle's."""
     rng = np.random.default_rng(1000 + round_)
     genomes = []
@@ -629,6 +630,9 @@ def test_randomized_populations(oracle, suite, round_):
             g[-1] = 4
             genomes.append(g)
     chunk = int(rng.choice([0, 64, 256, 1024, 4096, 16384]))
+    slice_kb = str(rng.choice(["", "16", "64", "256"]))
+    if slice_kb:
+        monkeypatch.setenv("LTGP_SLICE_KB", slice_kb)
     buf, offs, sizes = pack(genomes)
     exp = oracle.evaluate_population(buf, offs, sizes, suite, threads=0)
     with engine(suite, chunk=chunk) as e:
