@@ -298,6 +298,8 @@ struct Shard {
     uint32_t first = 0, count = 0;  // global slot range
     std::vector<Item> wl_items;                  // work-list scratch (host)
     std::vector<CombineTree> wl_ctrees;
+    std::vector<uint8_t> wl_tier;                // tapered tail: tier of each tree (0 = full-length chunks)
+    std::vector<uint64_t> wl_sorted;             // (size << 32 | tree) of the chunked trees, ascending
     bool kev_valid = false;         // kev bracket the last evaluation's k_eval
     TreeSet set[2];
     int cur = 0;
@@ -491,6 +493,30 @@ uint32_t xs_blocks(const XSlice* x, uint32_t G, std::vector<uint2>& blocks) {
     return t;
 }
 
+// Tapered tail of a resident work list (LTGP_TAPER = "f1,f2,f3": the share of
+// one grid wave given to chunks of C/2, C/4 and C/8 nodes; "0" = off).
+// The persistent grid ends with every warp inside its last item: with
+// full-length items that tail is one item's latency (config 3: 0.92 ms of a
+// 12.8 ms k_eval). The smallest chunked trees are cut into shorter chunks and
+// placed last, so the final items are short; small trees are chosen so no
+// tree's spine combine becomes the longest chain.
+struct Taper {
+    double f[3];
+    bool on;
+};
+static const Taper& taper_cfg() {
+    static const Taper v = [] {
+        Taper t{{0.5, 0.5, 0.5}, true};
+        if (const char* e = std::getenv("LTGP_TAPER")) {
+            t.f[0] = t.f[1] = t.f[2] = 0.0;
+            std::sscanf(e, "%lf,%lf,%lf", &t.f[0], &t.f[1], &t.f[2]);
+            t.on = t.f[0] > 0 || t.f[1] > 0 || t.f[2] > 0;
+        }
+        return t;
+    }();
+    return v;
+}
+
 // Evaluate every tree of `ts` on shard s: records (and optional per-case
 // outputs) land in rec/outs. Asynchronous on s.st.
 //
@@ -615,35 +641,79 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             // measured 2% faster, so they keep it. Two linear passes place
             // every item directly (no push_back, no sort).
             auto bucket = [](uint32_t n) { return 32 - __builtin_clz(n); };
-            // chunk counts by shift when Cg is a power of two (a 64-bit divide
-            // per tree and pass showed up in the per-generation host time)
+            // chunk counts by shift when the length is a power of two (a 64-bit
+            // divide per tree and pass showed up in the per-generation host time)
             const bool cg_pow2 = (Cg & (Cg - 1)) == 0;
-            const uint32_t cg_sh = (uint32_t)__builtin_ctz(Cg);
-            auto nchunks = [&](uint32_t n) { return cg_pow2 ? (n + Cg - 1) >> cg_sh : (n + Cg - 1) / Cg; };
-            uint32_t wcnt[33] = {}, ccnt[33] = {};
-            uint32_t nct_g = 0, nch_g = 0;
-            for (uint32_t t = tb[g]; t < tb[g + 1]; ++t) {
-                const uint32_t n = ts.h_size[t];
-                if (n <= Cg) { ++wcnt[bucket(n)]; continue; }
-                const uint32_t k = nchunks(n);
-                ++nct_g;
-                nch_g += k;
-                max_chunks = std::max(max_chunks, k);
-                ccnt[bucket(Cg)] += k - 1;
-                ++ccnt[bucket(n - (k - 1) * Cg)];
-            }
+            // Tapered tail (taper_cfg): tier k > 0 trees are cut into Cg >> k
+            // nodes per chunk and placed after the full-length chunks
+            std::vector<uint8_t>& tier = s.wl_tier;
+            tier.clear();
+            const uint32_t tier_c[4] = {Cg, Cg / 2, Cg / 4, Cg / 8};
+            auto clen = [&](uint32_t t) { return tier.empty() ? Cg : tier_c[tier[t]]; };
+            auto nchunks = [&](uint32_t n, uint32_t c) {
+                return cg_pow2 ? (n + c - 1) >> (uint32_t)__builtin_ctz(c) : (n + c - 1) / c;
+            };
+            uint32_t wcnt[33], ccnt[33], tcnt[4];
+            uint32_t nct_g, nch_g, nitems_g;
+            auto count_pass = [&] {
+                std::fill(wcnt, wcnt + 33, 0u);
+                std::fill(ccnt, ccnt + 33, 0u);
+                std::fill(tcnt, tcnt + 4, 0u);
+                nct_g = nch_g = 0;
+                for (uint32_t t = tb[g]; t < tb[g + 1]; ++t) {
+                    const uint32_t n = ts.h_size[t];
+                    if (n <= Cg) { ++wcnt[bucket(n)]; continue; }
+                    const uint32_t c = clen(t), k = nchunks(n, c);
+                    ++nct_g;
+                    nch_g += k;
+                    max_chunks = std::max(max_chunks, k);
+                    if (c != Cg) { tcnt[tier[t]] += k; continue; }
+                    ccnt[bucket(c)] += k - 1;
+                    ++ccnt[bucket(n - (k - 1) * c)];
+                }
+                nitems_g = nch_g;
+                for (int b = 0; b <= 32; ++b) nitems_g += wcnt[b];
+            };
+            count_pass();
             const uint32_t a0 = (uint32_t)all.size();
-            uint32_t nitems_g = nch_g;
-            for (int b = 0; b <= 32; ++b) nitems_g += wcnt[b];
             const uint64_t grid_warps = (uint64_t)std::max(s.eval_grid, 1) * kWarps;
             const bool lpt = G == 1 && (uint64_t)nitems_g <= 8 * grid_warps;
-            uint32_t cpos[33], wpos[33];
+            const Taper& tp = taper_cfg();
+            if (G == 1 && !lpt && tp.on && !e->chunk_fixed && cg_pow2 && Cg >= 8192) {
+                // the smallest chunked trees take the shortest chunks: ascending by
+                // size, tier 3 (Cg/8) first, each tier up to its share of a wave
+                std::vector<uint64_t>& sorted = s.wl_sorted;
+                sorted.clear();
+                for (uint32_t t = tb[g]; t < tb[g + 1]; ++t)
+                    if (ts.h_size[t] > Cg) sorted.push_back((uint64_t)ts.h_size[t] << 32 | t);
+                std::sort(sorted.begin(), sorted.end());
+                tier.assign(ts.count, 0);
+                size_t i = 0;
+                for (int k = 3; k >= 1 && i < sorted.size(); --k) {
+                    const uint64_t budget = (uint64_t)(tp.f[k - 1] * (double)grid_warps * tier_c[k]);
+                    uint64_t acc = 0;
+                    while (i < sorted.size() && acc + (sorted[i] >> 32) <= budget) {
+                        tier[(uint32_t)sorted[i]] = (uint8_t)k;
+                        acc += sorted[i] >> 32;
+                        ++i;
+                    }
+                }
+                count_pass();
+            }
+            uint32_t cpos[33], wpos[33], tpos[4] = {};
             uint32_t pos = a0, ccur = a0;
             if (lpt) {
                 for (int b = 32; b >= 0; --b) { cpos[b] = pos; pos += ccnt[b]; wpos[b] = pos; pos += wcnt[b]; }
             } else {
-                pos += nch_g;
-                for (int b = 32; b >= 0; --b) { wpos[b] = pos; pos += wcnt[b]; }
+                // full-length chunks in tree order, then by descending size class:
+                // whole trees, then the tier whose chunk length falls in the class
+                pos += nch_g - tcnt[1] - tcnt[2] - tcnt[3];
+                for (int b = 32; b >= 0; --b) {
+                    wpos[b] = pos;
+                    pos += wcnt[b];
+                    for (int k = 1; k <= 3; ++k)
+                        if (tcnt[k] && bucket(tier_c[k]) == b) { tpos[k] = pos; pos += tcnt[k]; }
+                }
             }
             all.resize(a0 + nitems_g);
             const uint32_t c0 = (uint32_t)ctrees.size();
@@ -655,11 +725,12 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
                     all[wpos[bucket(n)]++] = Item{t, kWholeTree, 0, n};
                     continue;
                 }
-                const uint32_t k = nchunks(n);
+                const uint32_t c = clen(t), k = nchunks(n, c);
                 ctrees[ci++] = CombineTree{t, nch, k, n};
                 for (uint32_t q = 0; q < k; ++q) {
-                    const uint32_t lo = q * Cg, hi = std::min(n, lo + Cg);
-                    all[lpt ? cpos[bucket(hi - lo)]++ : ccur++] = Item{t, nch + q, lo, hi};
+                    const uint32_t lo = q * c, hi = std::min(n, lo + c);
+                    uint32_t& at = c != Cg ? tpos[tier[t]] : lpt ? cpos[bucket(hi - lo)] : ccur;
+                    all[at++] = Item{t, nch + q, lo, hi};
                 }
                 nch += k;
             }

@@ -430,11 +430,23 @@ def test_config3_full_size_sampled(oracle, suite):
     buf, offs, sizes = ltgp.corpus(1, 4000, 4.0, 6.0)
     with engine(suite) as e:
         e.upload_packed(buf, offs, sizes)
-        rec = e.evaluate_population()
+        rec, outs = e.evaluate_outputs()
         rec2 = e.evaluate_population()
+        chunks = e.stats()["last_chunks"]
     assert rec.tobytes() == rec2.tobytes()  # determinism across launches
     exp = oracle.evaluate_population(buf, offs, sizes, suite, threads=0)
     assert_records_equal(rec, exp)
+    # The work list's tapered tail (11 waves of the persistent grid: the
+    # smallest chunked trees are cut into 8192/4096/2048-node chunks and run
+    # last) is in effect: more chunks than 16384-node chunks alone give, and
+    # the smallest chunked trees (the shortest chunks) match per case
+    big = sizes[sizes > 16384]
+    assert chunks > int(np.sum(-(-big.astype(np.int64) // 16384)))
+    order = np.argsort(sizes)
+    for k in order[sizes[order] > 16384][:3]:
+        g = np.ascontiguousarray(buf[int(offs[k]):int(offs[k]) + int(sizes[k])])
+        o, _ = oracle.eval_batch(g, suite[0], suite[2])
+        assert same_bits(outs[k], o)
 
 
 def test_streamed_evaluate_packed_matches_resident(oracle, suite):
