@@ -43,6 +43,7 @@ constexpr uint32_t kDefaultChunk = 16384;
 constexpr uint32_t kMaxSteps = 1024;
 constexpr uint32_t kMaxFrames = 256;
 constexpr uint32_t kMaxChunk = 1048576;    // automatic chunk length ceiling
+constexpr uint32_t kMaxWaveChunk = 1u << 22;  // ... of the one-wave rule for a few huge trees (launch_eval)
 constexpr uint32_t kSpillFrames = 1024;  // per warp; items that need more are re-run
 constexpr int kRerunCtas = 8;
 
@@ -593,12 +594,22 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             // chunks cost more than the fuller last wave gains (4.33 vs 4.62
             // ms per evaluation without the rule there).
             if (k0 > W / 2 && waves <= 8 && C >= 2048 && big_trees <= 512) {
-                uint32_t lo = std::max<uint32_t>(1024, C / 2) / 1024, hi = C / 1024;  // in units of 1024
-                while (lo < hi) {  // smallest c with chunks_of(c) <= waves * W (non-increasing in c)
+                // k_eval's time does not depend on the chunk length while the
+                // grid stays full, and the sequential combine shrinks like
+                // 1/sqrt(C) (spine steps), so the best length is the one that
+                // gives every warp exactly ONE chunk: 48 x 4e8 nodes at 4082688
+                // instead of 1015808 (4 waves): k_eval 312 vs 310 ms, combine
+                // 19.2 vs 37.4 ms; 48 x 1e7 at 102400 instead of 51200:
+                // 12.7 vs 14.1 ms per evaluation. Half a wave (twice that
+                // length) doubles k_eval. Above kMaxWaveChunk the fewest waves
+                // that length allows, shortened as before.
+                const uint64_t w = std::max<uint64_t>(1, (chunks_of(kMaxWaveChunk) + W - 1) / W);
+                uint32_t lo = 1, hi = kMaxWaveChunk / 1024;  // in units of 1024
+                while (lo < hi) {  // smallest c with chunks_of(c) <= w * W (non-increasing in c)
                     const uint32_t mid = (lo + hi) / 2;
-                    if (chunks_of(mid * 1024) <= waves * W) hi = mid; else lo = mid + 1;
+                    if (chunks_of(mid * 1024) <= w * W) hi = mid; else lo = mid + 1;
                 }
-                C = hi * 1024;
+                C = std::max<uint32_t>(hi * 1024, std::max<uint32_t>(1024, C / 2));
             }
         }
         // chunk summaries are sized exactly by k_plan (PlanPool); these are
@@ -2247,6 +2258,7 @@ static int gen_device_launch(ltgp_engine* e, const ltgp_plan* plans, uint32_t M)
     ga.fixed_chunk = e->chunk_fixed ? e->chunk : 0u;
     ga.default_chunk = kDefaultChunk;
     ga.max_chunk = kMaxChunk;
+    ga.max_wave_chunk = kMaxWaveChunk;
     ga.grid_warps = (uint32_t)s.eval_grid * kWarps;
     ga.st = st;
     PlanPool pool{};

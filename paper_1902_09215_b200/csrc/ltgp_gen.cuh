@@ -59,7 +59,7 @@ struct GenArgs {
     CombineTree* ctrees;
     uint32_t chunks_cap;        // chunk summaries the per-chunk buffers hold
     uint32_t fixed_chunk;       // 0: automatic chunk length
-    uint32_t default_chunk, max_chunk;
+    uint32_t default_chunk, max_chunk, max_wave_chunk;
     uint32_t grid_warps;        // k_eval's persistent warps
     GenStatus* st;
 };
@@ -207,12 +207,15 @@ __global__ void __launch_bounds__(1024) k_gen_control(GenArgs a) {
         const unsigned long long k0 = chunks_of(C, &big_trees);
         const unsigned long long waves = (k0 + W - 1) / W;
         if (k0 > W / 2 && waves <= 8 && C >= 2048 && big_trees <= 512) {
-            uint32_t lo = max(1024u, C / 2) / 1024, hi = C / 1024;
+            // one chunk per warp where max_wave_chunk allows it, else the fewest waves
+            const unsigned long long kw = chunks_of(a.max_wave_chunk, nullptr);
+            const unsigned long long w = max(1ull, (kw + W - 1) / W);
+            uint32_t lo = 1, hi = a.max_wave_chunk / 1024;
             while (lo < hi) {
                 const uint32_t mid = (lo + hi) / 2;
-                if (chunks_of(mid * 1024, nullptr) <= waves * W) hi = mid; else lo = mid + 1;
+                if (chunks_of(mid * 1024, nullptr) <= w * W) hi = mid; else lo = mid + 1;
             }
-            C = hi * 1024;
+            C = max(hi * 1024, max(1024u, C / 2));
         }
     }
     // 3. counts per bucket, chunk ids and combine-tree indices in tree order

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--check", type=int, default=2)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--chunk", type=int, default=0)
+    ap.add_argument("--chunks", default="", help="comma list of chunk lengths to time on the same trees (a sweep)")
     ap.add_argument("--ops", default="",
                     help="remap function opcodes (e.g. '0120': division -> add) to study the op mix")
     ap.add_argument("--cpu-trees", type=int, default=0,
@@ -37,6 +38,18 @@ def main():
         lut[:4] = [int(c) for c in a.ops]
         trees = [lut[g] for g in trees]
     suite = ltgp.make_suite(ltgp.suite_seed(1))
+    for c in [int(x) for x in a.chunks.split(",") if x][:-1]:
+        with ltgp.Engine([0], node_limit=2**62, chunk_nodes=c) as e:
+            e.set_suite(*suite)
+            e.upload_population(trees)
+            for _ in range(a.reps):
+                e.evaluate_population()
+                st = e.stats()
+                print(f"chunk {c}: eval {st['eval_seconds']*1e3:.1f} ms (k_eval {st['keval_seconds']*1e3:.1f}, combine "
+                      f"{st['combine_seconds']*1e3:.1f}) {a.trees*n*48/st['eval_seconds']/1e12:.3f} T GPops/s, chunks "
+                      f"{st['last_chunks']}, reruns {st['last_fallback_items']}, spine steps {st['last_spine_steps']}", flush=True)
+    if a.chunks:
+        a.chunk = int(a.chunks.split(",")[-1])
     with ltgp.Engine([0], node_limit=2**62, chunk_nodes=a.chunk) as e:
         e.set_suite(*suite)
         e.upload_population(trees)
