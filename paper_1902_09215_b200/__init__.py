@@ -22,7 +22,8 @@ from typing import Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-CUDA_LIB_PATH = os.path.join(_PKG, "libltgp_cuda.so")
+# (LTGP_CUDA_LIB: a kernel variant from tools/build_variant.py, for experiments)
+CUDA_LIB_PATH = os.environ.get("LTGP_CUDA_LIB") or os.path.join(_PKG, "libltgp_cuda.so")
 HOST_LIB_PATH = os.path.join(_PKG, "libltgp_host.so")
 
 LANES = 48

@@ -63,6 +63,16 @@ def _deps(dirname, exts):
     return out
 
 
+def patch_jump_tables(lib: str, verbose: bool = False) -> None:
+    """Post-build step on a freshly linked libltgp_cuda.so (patch_jt.py): fails
+    the build if the interpreter's dispatch sites do not end up on one table."""
+    if PKG not in sys.path:
+        sys.path.insert(0, PKG)
+    import patch_jt
+    patch_jt.patch(lib, verbose=verbose)
+    patch_jt.verify(lib)
+
+
 def build(force: bool = False, verbose: bool = False) -> None:
     nvcc = os.environ.get("NVCC", "nvcc")
     cu_deps = _deps(CSRC, (".cu", ".cuh", ".h")) + [os.path.join(ROOT, "include", "ltgp_cuda.h")]
@@ -71,6 +81,8 @@ def build(force: bool = False, verbose: bool = False) -> None:
         _run(["g++", *CXX_FLAGS, "-c", "-o", PACK_OBJ, PACK_SRC])
         _run([nvcc, *NVCC_FLAGS, "-shared", "-o", CUDA_LIB, os.path.join(CSRC, "ltgp_engine.cu"), PACK_OBJ],
              log=os.path.join(CSRC, "ptxas.log"))
+        # the direct-threaded interpreter's jump-table copies become one (see patch_jt.py)
+        patch_jump_tables(CUDA_LIB, verbose)
     host_deps = _deps(HOST, (".cpp", ".hpp")) + [os.path.join(ROOT, "include", "ltgp_host.h"), CUDA_LIB]
     if force or _stale(HOST_LIB, host_deps):
         _run(["g++", *CXX_FLAGS, "-shared", "-o", HOST_LIB, os.path.join(HOST, "ltgp_host.cpp"),

@@ -16,4 +16,5 @@ os.makedirs(out, exist_ok=True)
 B._run(["g++", *B.CXX_FLAGS, "-c", "-o", os.path.join(out, "ltgp_pack.o"), B.PACK_SRC])
 B._run(["nvcc", *B.NVCC_FLAGS, *extra, "-shared", "-o", os.path.join(out, "libltgp_cuda.so"),
         os.path.join(B.CSRC, "ltgp_engine.cu"), os.path.join(out, "ltgp_pack.o")], log=os.path.join(out, "ptxas.log"))
+B.patch_jump_tables(os.path.join(out, "libltgp_cuda.so"), verbose=True)
 print("built", out)
