@@ -301,12 +301,14 @@ def run_ours(args, rank, world, local_rank):
             pj = json.load(open(prof))
             traffic = pj.get("dram_bytes_per_launch")
             mp = pj.get("metrics_pct", {})
-            # what actually bounds the interpreter: issue
-            # slots and the shared-memory pipe, not the FP32 pipe or HBM
+            # what actually bounds the interpreter: the
+            # shared-memory pipe, the per-pair indirect branch and issue
+            # slots, not the FP32 pipe or HBM
             binding = {
-                "resource": "latency of the interpreter's per-pair dispatch chain (LDS record -> jump-table LDC -> "
-                            "BRX): 41% of k_eval's stall samples (profiles/r01_keval_stalls.txt); throughput follows "
-                            "resident warps; issue and shared-memory pipe shown below are not saturated",
+                "resource": "the shared-memory data pipe (a 48-case frame is 2 wavefronts per stack access, 3.2 per "
+                            "node) and the per-pair indirect branch: with the direct-threaded dispatch the stall "
+                            "samples (profiles/r02c_keval_stalls.txt) are branch resolution 22%, shared-memory "
+                            "scoreboard 20%, fixed-latency dependencies 18%; issue slots ~70% busy",
                 "issue_active_pct": float(mp.get("sm__issue_active.avg.pct_of_peak_sustained_elapsed", "nan")),
                 "shared_wavefronts_pct": float(mp.get(
                     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "nan")),
