@@ -47,6 +47,21 @@ def test_cubin_is_sm100a():
     assert "sm_100a" in out
 
 
+def test_interpreter_dispatch_sites_share_one_jump_table():
+    """The build's post-link step (paper_1902_09215_b200/patch_jt.py) folded
+    the direct-threaded interpreter's per-site jump tables into one: every
+    k_eval variant in the shipped library has all its dispatch sites on a
+    single table (an unpatched library computes the same results 3x slower)."""
+    import sys
+    sys.path.insert(0, os.path.dirname(ltgp.CUDA_LIB_PATH))
+    import patch_jt
+    patch_jt.verify(ltgp.CUDA_LIB_PATH)
+    info = patch_jt._analyse(ltgp.CUDA_LIB_PATH)
+    assert len(info) == 2  # resident and cross-slice k_eval
+    for kern, where, group, others in info:
+        assert len(group) >= 28 and len({t for _, t in group}) == 1, kern
+
+
 def test_no_gpu_fails_loudly():
     import torch
     if torch.cuda.is_available():
