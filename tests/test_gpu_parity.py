@@ -498,8 +498,11 @@ def test_streamed_packed_transfer(oracle, suite, monkeypatch):
         buf[end:nxt] = rng.integers(0, 256, nxt - end)
     exp = oracle.evaluate_population(buf, offs, sizes, suite, threads=0)
     results = []
-    for env in ({"LTGP_PACK": "0"}, {}, {"LTGP_SLICES": "64", "LTGP_SLICE_KB": "1"}, {"LTGP_PACK_THREADS": "3"}):
-        for k in ("LTGP_PACK", "LTGP_SLICES", "LTGP_SLICE_KB", "LTGP_PACK_THREADS"):
+    # (LTGP_XSLICE=0: per-slice launches, k_decode_packed / k_decode + k_plan_warp<false>,
+    # the path a profiler or sanitizer gets)
+    for env in ({"LTGP_PACK": "0"}, {}, {"LTGP_SLICES": "64", "LTGP_SLICE_KB": "1"}, {"LTGP_PACK_THREADS": "3"},
+                {"LTGP_XSLICE": "0", "LTGP_SLICE_KB": "8"}, {"LTGP_XSLICE": "0", "LTGP_PACK": "0", "LTGP_SLICE_KB": "8"}):
+        for k in ("LTGP_PACK", "LTGP_SLICES", "LTGP_SLICE_KB", "LTGP_PACK_THREADS", "LTGP_XSLICE"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
@@ -516,7 +519,8 @@ def test_streamed_packed_transfer(oracle, suite, monkeypatch):
     assert len({r[:2] for r in results}) == 1
     assert results[0][2] <= buf.size and results[1][2] < results[0][2]
     # config-3 corpus: ~0.63 bytes a node cross PCIe, records unchanged
-    monkeypatch.delenv("LTGP_PACK_THREADS")
+    for k in ("LTGP_PACK", "LTGP_SLICES", "LTGP_SLICE_KB", "LTGP_PACK_THREADS", "LTGP_XSLICE"):
+        monkeypatch.delenv(k, raising=False)
     cb, co, cs = ltgp.corpus(1, 400, 4.0, 5.0)
     with engine(suite) as e:
         e.upload_packed(cb, co, cs)
