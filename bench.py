@@ -302,13 +302,14 @@ def run_ours(args, rank, world, local_rank):
             traffic = pj.get("dram_bytes_per_launch")
             mp = pj.get("metrics_pct", {})
             # what actually bounds the interpreter: the
-            # shared-memory pipe, the per-pair indirect branch and issue
-            # slots, not the FP32 pipe or HBM
+            # per-pair dependent chain (indirect branch, operand loads) and
+            # issue slots, not the FP32 pipe or HBM
             binding = {
-                "resource": "the shared-memory data pipe (a 48-case frame is 2 wavefronts per stack access, 3.2 per "
-                            "node) and the per-pair indirect branch: with the direct-threaded dispatch the stall "
-                            "samples (profiles/r02c_keval_stalls.txt) are branch resolution 22%, shared-memory "
-                            "scoreboard 20%, fixed-latency dependencies 18%; issue slots ~70% busy",
+                "resource": "latency of each warp's per-pair chain at 32 resident warps: with the direct-threaded "
+                            "dispatch the stall samples (profiles/r02c_keval_stalls.txt) are branch resolution "
+                            "after the handler's BRX 22% (+9% instruction fetch at its target), shared-memory "
+                            "scoreboard 20%, fixed-latency dependencies 18%; issue slots ~70% busy; the "
+                            "shared-memory pipe (83%) does not bind yet (broadcast-leaf probe, DESIGN.md 3.9)",
                 "issue_active_pct": float(mp.get("sm__issue_active.avg.pct_of_peak_sustained_elapsed", "nan")),
                 "shared_wavefronts_pct": float(mp.get(
                     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "nan")),
