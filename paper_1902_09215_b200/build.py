@@ -76,7 +76,7 @@ def patch_jump_tables(lib: str, verbose: bool = False) -> None:
 def build(force: bool = False, verbose: bool = False) -> None:
     nvcc = os.environ.get("NVCC", "nvcc")
     cu_deps = _deps(CSRC, (".cu", ".cuh", ".h")) + [os.path.join(ROOT, "include", "ltgp_cuda.h")]
-    cu_deps += [PACK_SRC]
+    cu_deps += [PACK_SRC, os.path.join(PKG, "patch_jt.py")]
     if force or _stale(CUDA_LIB, cu_deps):
         _run(["g++", *CXX_FLAGS, "-c", "-o", PACK_OBJ, PACK_SRC])
         _run([nvcc, *NVCC_FLAGS, "-shared", "-o", CUDA_LIB, os.path.join(CSRC, "ltgp_engine.cu"), PACK_OBJ],
