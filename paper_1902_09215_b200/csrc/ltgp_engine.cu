@@ -579,12 +579,13 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             };
             // chunks at C (C is a power of two here: shifts) and the trees
             // that get chunked, in one pass
-            uint64_t k0 = 0, big_trees = 0;
+            uint64_t k0 = 0, big_trees = 0, big_nodes = 0;
             {
                 const uint32_t sh = (uint32_t)__builtin_ctz(C);
                 for (uint32_t t = 0; t < ts.count; ++t)
                     if (ts.h_size[t] > C) {
                         k0 += ((uint64_t)ts.h_size[t] + C - 1) >> sh;
+                        big_nodes += ts.h_size[t];
                         ++big_trees;
                     }
             }
@@ -593,7 +594,12 @@ int launch_eval(ltgp_engine* e, Shard& s, TreeSet& ts, bool want_outs) {
             // chunked trees (an evolved generation 3000: 3000+) the shorter
             // chunks cost more than the fuller last wave gains (4.33 vs 4.62
             // ms per evaluation without the rule there).
-            if (k0 > W / 2 && waves <= 8 && C >= 2048 && big_trees <= 512) {
+            // (Also when the chunks fill less than half a wave but the chunked
+            // trees hold most of the nodes, e.g. the 6 trees one of 8 GPUs gets
+            // of config 4: the power of two above `want` is up to twice too
+            // long there, and C / 2, the floor below, measured best: 6 x 4e8
+            // nodes at 524288 instead of 1048576, 94 vs 118 ms.)
+            if ((k0 > W / 2 || big_nodes * 2 >= total) && waves <= 8 && C >= 2048 && big_trees <= 512) {
                 // k_eval's time does not depend on the chunk length while the
                 // grid stays full, and the sequential combine shrinks like
                 // 1/sqrt(C) (spine steps), so the best length is the one that

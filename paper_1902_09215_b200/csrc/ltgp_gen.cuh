@@ -192,28 +192,30 @@ __global__ void __launch_bounds__(1024) k_gen_control(GenArgs a) {
         while (C < a.default_chunk && (unsigned long long)C * 4 <= per * 3) C *= 2;
         const double want = pow(1.25 * (double)biggest, 2.0 / 3.0);
         while (C < a.max_chunk && (double)C < want) C *= 2;
-        auto chunks_of = [&](uint32_t c, uint32_t* big) {
-            unsigned long long k = 0;
+        auto chunks_of = [&](uint32_t c, uint32_t* big, unsigned long long* bign) {
+            unsigned long long k = 0, bn = 0;
             uint32_t b = 0;
             for (uint32_t t = threadIdx.x; t < M; t += 1024) {
                 const uint32_t n = a.child_size[t];
-                if (n > c) { k += (n + c - 1) / c; ++b; }
+                if (n > c) { k += (n + c - 1) / c; ++b; bn += n; }
             }
             k = gen_sum<unsigned long long>(k, w64);
             if (big) *big = gen_sum<uint32_t>(b, w32);
+            if (bign) *bign = gen_sum<unsigned long long>(bn, w64);
             return k;
         };
         uint32_t big_trees = 0;
-        const unsigned long long k0 = chunks_of(C, &big_trees);
+        unsigned long long big_nodes = 0;
+        const unsigned long long k0 = chunks_of(C, &big_trees, &big_nodes);
         const unsigned long long waves = (k0 + W - 1) / W;
-        if (k0 > W / 2 && waves <= 8 && C >= 2048 && big_trees <= 512) {
+        if ((k0 > W / 2 || big_nodes * 2 >= nodes) && waves <= 8 && C >= 2048 && big_trees <= 512) {
             // one chunk per warp where max_wave_chunk allows it, else the fewest waves
-            const unsigned long long kw = chunks_of(a.max_wave_chunk, nullptr);
+            const unsigned long long kw = chunks_of(a.max_wave_chunk, nullptr, nullptr);
             const unsigned long long w = max(1ull, (kw + W - 1) / W);
             uint32_t lo = 1, hi = a.max_wave_chunk / 1024;
             while (lo < hi) {
                 const uint32_t mid = (lo + hi) / 2;
-                if (chunks_of(mid * 1024, nullptr) <= w * W) hi = mid; else lo = mid + 1;
+                if (chunks_of(mid * 1024, nullptr, nullptr) <= w * W) hi = mid; else lo = mid + 1;
             }
             C = max(hi * 1024, max(1024u, C / 2));
         }
